@@ -1,0 +1,219 @@
+/*
+ * embrace.h — C ABI of the B200-native EmbRace sparse-embedding exchange.
+ *
+ * The method: EmbRace "Sparsity-aware Hybrid Communication" (arXiv 2110.09132,
+ * /root/reference/PAPER.md) — an [L, D] embedding table column-partitioned over
+ * N GPUs (§4.1.2), a forward AlltoAll of lookup results and a
+ * backward AlltoAll of sparse gradients (§4.1.1/§4.1.3,
+ * Fig. 3 caption PAPER.md:262), the vertical split of the coalesced sparse
+ * gradient into a prior and a scheduled part (Alg. 1), the
+ * modified sparse Adam and a priority-ordered AllReduce
+ * queue for dense gradients.
+ *
+ * Conventions (every call):
+ *   - Return emb_status; EMB_OK == 0.  No exceptions, no abort.
+ *   - Host-side argument checks fail BEFORE anything is enqueued.
+ *   - Device-detected errors (id out of range, prefetched-id mismatch, P2P
+ *     wait timeout) set a sticky device flag, reported by emb_get_stats and
+ *     emb_flush.  CUDA / NCCL errors poison the context: every later call
+ *     returns the same code.
+ *   - "device" pointers are CUDA device pointers on the context's device;
+ *     "host" pointers are ordinary host memory.  cudaStream_t / cudaEvent_t
+ *     are passed as opaque handles (emb_stream_t / emb_event_t).
+ *   - One context per rank (one process per GPU).  A context is not
+ *     thread-safe.
+ *   - Call order: emb_create -> emb_ipc_handle -> (exchange handles over the
+ *     process group) -> emb_shard_init -> (emb_forward_exchange ->
+ *     emb_backward_exchange)* -> emb_flush -> emb_shard_destroy.
+ *
+ * Ownership: the library owns the partitioned state — the column shard
+ * [L, D/N], the Adam moments and the NVLink-visible exchange buffers — in
+ * device memory it allocates itself, because peers read the shard and write
+ * the receive buffers through CUDA IPC mappings.
+ * emb_state_ptr exposes them (for checkpointing and tests).  Everything else
+ * (ids, outputs, output gradients, dense buffers, events) is caller-owned and
+ * borrowed only for the duration of the stream work the call enqueues.
+ */
+#ifndef EMBRACE_H
+#define EMBRACE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMB_MAX_WORLD 8
+#define EMB_IPC_HANDLE_BYTES 64
+#define EMB_UNIQUE_ID_BYTES 128
+
+typedef struct CUstream_st* emb_stream_t; /* == cudaStream_t */
+typedef struct CUevent_st* emb_event_t;   /* == cudaEvent_t  */
+
+typedef enum {
+  EMB_OK = 0,
+  EMB_ERR_INVALID_ARG = 1, /* NULL / negative / unknown enum                        */
+  EMB_ERR_SHAPE = 2,       /* D % N != 0, (D/N)*e % 16 != 0, N > D, N > 8            */
+  EMB_ERR_ID_RANGE = 3,    /* a token id < 0 or >= L (device-detected, sticky)       */
+  EMB_ERR_CAPACITY = 4,    /* n > max_tokens, or the per-source sort does not fit     */
+  EMB_ERR_STATE = 5,       /* call order; ids of forward(t+1) != next_ids of bwd(t)  */
+  EMB_ERR_CUDA = 6,
+  EMB_ERR_NCCL = 7,
+  EMB_ERR_TIMEOUT = 8      /* a bounded wait on a peer flag expired (sticky)         */
+} emb_status;
+
+typedef enum { EMB_FP32 = 0, EMB_BF16 = 1 } emb_dtype; /* table, wire and output dtype */
+typedef enum { EMB_SGD = 0, EMB_ADAM = 1 } emb_optim;
+/* Backward modes (reading R2):
+ *   RAW   — plain hybrid communication: uncoalesced dY column slices travel,
+ *           the owner coalesces;
+ *   COAL  — the sender coalesces (Alg. 1 line 2), one exchange;
+ *   SPLIT — the sender coalesces and Alg. 1 splits the rows into the prior
+ *           part (rows the next batch reads, exchanged + applied on the
+ *           caller's stream) and the scheduled part (exchanged + applied on a
+ *           low-priority side stream, finished before forward(t+2) or flush). */
+typedef enum { EMB_BWD_RAW = 0, EMB_BWD_COAL = 1, EMB_BWD_SPLIT = 2 } emb_bwd_mode;
+
+typedef struct {
+  int64_t vocab;        /* L                                                       */
+  int32_t dim;          /* D (full embedding width)                                 */
+  int32_t world;        /* N, 1..8                                                  */
+  int32_t rank;         /* r, 0..N-1                                                */
+  int32_t device;       /* CUDA device ordinal of this rank                         */
+  emb_dtype dtype;      /* storage / wire / output dtype; math is fp32              */
+  int32_t max_tokens;   /* capacity: tokens per rank per iteration                  */
+  emb_bwd_mode mode;
+  emb_optim optim;
+  float lr, beta1, beta2, eps;
+  float grad_scale;     /* multiplies the summed sparse gradient; 0 => 1/N (R5)    */
+  int64_t pad_id;       /* -1: pad is an ordinary id; >= 0: its gradient is dropped */
+  int32_t queue_window; /* dense queue window W >= 1 (reading R16)                  */
+  int32_t timeout_ms;   /* bound on every peer-flag wait; 0 => 10000                */
+} emb_config;
+
+typedef struct {
+  int64_t iter;                          /* completed backward calls             */
+  int32_t world;
+  int32_t n_tokens[EMB_MAX_WORLD];       /* T_s of the last iteration            */
+  int32_t u[EMB_MAX_WORLD];              /* |unique grad ids| per source         */
+  int32_t p[EMB_MAX_WORLD];              /* prior rows per source (Alg. 1 l.4)   */
+  int32_t q[EMB_MAX_WORLD];              /* scheduled rows per source (l.5)      */
+  /* cumulative bytes this rank moved, per peer (self included for reference;
+   * algorithmic counts taken in the kernels that move them):                  */
+  int64_t fwd_bytes_pulled[EMB_MAX_WORLD]; /* lookup slices read from peer s's shard */
+  int64_t bwd_bytes_pushed[EMB_MAX_WORLD]; /* gradient slices written to owner s     */
+  int64_t ids_bytes_pushed[EMB_MAX_WORLD]; /* token ids written to peer s            */
+  int32_t err_flags;                     /* sticky device flags: 1 id range, 2 state, 4 timeout */
+} emb_stats;
+
+/* Debug items for emb_debug_copy (integer parity tests). `src` selects the
+ * source rank n where it applies.  All copies are synchronous.              */
+typedef enum {
+  EMB_DBG_GIDS = 0,     /* int32 [T_src]  gathered ids of source src (iteration of the last bwd) */
+  EMB_DBG_SLOT_IDS = 1, /* int32 [u_src]  source src's unique grad ids in slot order:
+                           prior part ascending, then scheduled part ascending      */
+  EMB_DBG_COUNTS = 2,   /* int32 [4*N]    per source: T, u, p, nchunks               */
+  EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src stably sorted by id */
+  EMB_DBG_ISSUE_LOG = 4 /* int64 [k]      dense-queue tickets in issue order          */
+} emb_debug_item;
+
+typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1, EMB_STATE_ADAM_V = 2 } emb_state_item;
+
+typedef struct emb_ctx emb_ctx;
+
+const char* emb_status_str(emb_status s);
+
+/* Device bytes the context will allocate (symmetric + local), for capacity
+ * planning; no allocation happens.                                           */
+emb_status emb_workspace_bytes(const emb_config* cfg, size_t* symmetric_bytes, size_t* local_bytes);
+
+/* Validate cfg, select cfg->device, allocate the library-owned state and
+ * streams.  No communication.  The shard is not initialised yet.             */
+emb_status emb_create(const emb_config* cfg, emb_ctx** out);
+
+/* CUDA IPC handle (EMB_IPC_HANDLE_BYTES) of this rank's NVLink-visible
+ * region; the caller all-gathers the N handles over its process group.       */
+emb_status emb_ipc_handle(emb_ctx* ctx, uint8_t* handle_out);
+
+/* NCCL unique id (EMB_UNIQUE_ID_BYTES) for the dense-gradient queue; call on
+ * rank 0 and broadcast.                                                      */
+emb_status emb_get_unique_id(uint8_t* id_out);
+
+/* a0 of SURVEY §8(a): shard init ("partitioned into processes
+ * before the training start").
+ *   peer_handles : host, N * EMB_IPC_HANDLE_BYTES, rank order (own ignored)
+ *   nccl_id      : host, EMB_UNIQUE_ID_BYTES, or NULL (no dense queue)
+ *   shard_init   : device [L, D/N] row-major in cfg->dtype — this rank's
+ *                  columns W[:, r*D/N:(r+1)*D/N]; copied (caller keeps it)
+ * Adam moments are zeroed and the step counter reset.  Collective: all N
+ * ranks must call it (it rendezvous on NCCL when nccl_id != NULL).          */
+emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8_t* nccl_id,
+                          const void* shard_init, emb_stream_t stream);
+
+/* a1-a4 of SURVEY §8(a): forward exchange of iteration t.
+ *   ids : device int32 [n]  this rank's token ids (0 <= id < L)
+ *   n   : 0 <= n <= max_tokens
+ *   out : device [n, D] row-major in cfg->dtype — full embedding rows
+ *         out[j, :] = W[ids[j], :] (every column slice pulled from its owner)
+ * Enqueued on `stream`; `out` is valid when the stream reaches the end of
+ * this call's work.  If the previous backward received next_ids, `ids` must
+ * equal them (checked on device -> EMB_ERR_STATE flag).  Collective.        */
+emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, void* out,
+                                emb_stream_t stream);
+
+/* a5-a12 of SURVEY §8(a): backward exchange of iteration t (Alg. 1 and
+ * PAPER.md:280 "AlltoAll is called again to exchange sparse gradients").
+ *   grad_out : device [n, D] in cfg->dtype, gradient of the last forward's
+ *              `out` (same n and ids); borrowed until `stream` completes
+ *   next_ids : device int32 [n_next], the ids this rank will pass to the next
+ *              forward (the paper's prefetch), or NULL on the
+ *              last step (D_next = empty: every row is scheduled, reading R8)
+ * Every shard row in U = unique(all ranks' ids, pad dropped if pad_id >= 0)
+ * receives one optimizer step with g = grad_scale * sum over ranks of its dY
+ * rows.  SPLIT: rows in D_next are updated on `stream`; the rest on the side
+ * stream, complete before forward(t+2) and at emb_flush.  Collective.       */
+emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32_t* next_ids,
+                                 int32_t n_next, emb_stream_t stream);
+
+/* a13: dense-gradient AllReduce priority queue.
+ *   buf      : device [count] (fp32 or bf16), averaged in place over ranks
+ *   priority : lower = sooner (dense blocks in FP order; reading R16)
+ *   ready    : event the producer recorded after this block's backward, or NULL
+ *   ticket   : out, id for dense_wait
+ * Issue rule (identical on every rank, a pure function of the enqueue
+ * sequence): after each enqueue, while >= W requests are pending, issue the
+ * smallest (priority, seq).  Requires nccl_id at shard init.               */
+emb_status dense_allreduce_enqueue(emb_ctx* ctx, void* buf, int64_t count, emb_dtype dtype,
+                                   int32_t priority, emb_event_t ready, int64_t* ticket);
+/* Issue every pending request in (priority, seq) order.                      */
+emb_status dense_queue_flush(emb_ctx* ctx);
+/* Make `consumer` wait for the AllReduce of `ticket` (must be issued).       */
+emb_status dense_wait(emb_ctx* ctx, int64_t ticket, emb_stream_t consumer);
+
+/* Make `stream` wait for all outstanding deferred work (scheduled parts) and
+ * the dense queue, then synchronise it; returns the sticky device error as a
+ * status (EMB_ERR_ID_RANGE / STATE / TIMEOUT) if one was raised.           */
+emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream);
+
+/* Synchronise the device and read the counters of the last iteration.       */
+emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out);
+
+/* Synchronous copy of an integer intermediate (see emb_debug_item) into host
+ * memory of `cap` bytes; *n receives the element count.                    */
+emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, size_t cap, size_t* n);
+
+/* Device pointer of library-owned state ([L, D/N]; shard in cfg->dtype, Adam
+ * moments fp32).  Valid until emb_shard_destroy.                            */
+emb_status emb_state_ptr(emb_ctx* ctx, int32_t item, void** ptr);
+
+/* Pure host function of the dense-queue issue rule (reading R16), exposed so
+ * the rule can be checked without a GPU: out[i] = seq issued i-th.          */
+emb_status emb_queue_issue_order(const int32_t* priorities, int32_t n, int32_t window, int32_t* out);
+
+emb_status emb_shard_destroy(emb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMBRACE_H */

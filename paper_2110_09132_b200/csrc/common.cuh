@@ -1,0 +1,196 @@
+// common.cuh — device-side layout, context and primitives shared by the
+// EmbRace exchange kernels (sm_100a).  Product code: never includes or links
+// anything from oracle/.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define EMB_WMAX 8
+
+namespace emb {
+
+enum Mode { RAW = 0, COAL = 1, SPLIT = 2 };
+enum Optim { SGD = 0, ADAM = 1 };
+enum DType { F32 = 0, BF16 = 1 };
+enum ErrBit { ERR_ID = 1, ERR_STATE = 2, ERR_TIMEOUT = 4 };
+
+// Peer-written flags living in every rank's NVLink-visible region.  Slot [n]
+// is written only by rank n (epoch values = iteration number t, monotone).
+struct Flags {
+  uint32_t ids[EMB_WMAX];         // ids of iteration v are in my gids[v&1][n]
+  uint32_t pub[2][EMB_WMAX];      // part 0 (prior / all) / part 1 (scheduled) rows of iteration v
+                                  // from sender n are in my recv[v&1][n]
+  uint32_t prior_done[EMB_WMAX];  // owner n applied the prior part of iteration v
+  uint32_t def_done[EMB_WMAX];    // owner n applied the scheduled part of iteration v
+  uint32_t boot[EMB_WMAX];        // rank n finished emb_shard_init (its shard is loaded)
+  uint32_t pad[64 - 6 * EMB_WMAX];
+};
+
+// Byte offsets inside the symmetric (IPC-exported) region; identical on every rank.
+struct SymLayout {
+  size_t shard;   // [L][d]            table dtype     (peers read: forward pull)
+  size_t gids;    // [2][N][max_tok]   int32           (peers write: id all-gather)
+  size_t ntok;    // [2][N]            int32
+  size_t recv;    // [2][N][max_tok][d] wire = table dtype (senders write: grad AlltoAll)
+  size_t flags;   // Flags
+  size_t total;
+};
+
+// Everything a kernel needs, passed by value.
+struct DevCtx {
+  int N, r;
+  long long L;
+  int D, d, esz;          // esz: bytes per element of the table dtype
+  int dtype, mode, optim;
+  int max_tok;
+  int cpr, cps;           // 16-byte chunks per full row (D*esz/16) / per column slice (d*esz/16)
+  long long pad_id;
+  float lr, beta1, beta2, eps, scale;
+  unsigned long long timeout_ns;
+  int C;                  // rows per reduce chunk
+  int max_chunks;         // per source per parity
+  int idbits, posbits;
+
+  char* sym[EMB_WMAX];    // base of every rank's symmetric region (own included)
+  SymLayout lay;
+
+  // local (not peer-visible)
+  float* adam_m;          // [L][d]
+  float* adam_v;          // [L][d]
+  int* nextmark;          // [L]       epoch tag: id in D_next of iteration v  <=> nextmark[id] == v+1
+  unsigned long long* slotmap;  // [L][N] (t << 32) | slot  — source n holds id in slot k at iteration t
+  int* perm;              // [2][N][max_tok]    positions sorted by (id, pos)
+  int* slot_id;           // [2][N][max_tok]    slot k -> id   (prior asc, then scheduled asc)
+  int* seg_start;         // [2][N][max_tok]    slot k -> first index into perm
+  int* seg_end;           // [2][N][max_tok]    slot k -> one past last
+  int* chunk_off;         // [2][N][max_tok+1]  slot k -> first chunk
+  int* chunk_slot;        // [2][N][max_chunks] chunk -> slot
+  int* counts;            // [2][N][4]          T, u, p (prior slots), nchunks
+  int* slot_ctr;          // [2][N][max_tok]    arrivals of multi-chunk slots
+  float* scratch;         // [2][N][max_chunks][dw]  multi-chunk partials (dw = D for sender, d for RAW owner)
+  char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (wire dtype)
+  float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
+  unsigned int* done_ctr; // [32]  last-block counters, one per kernel kind
+  unsigned int* t_rec;    // [2]   t of the iteration using parity p
+  int* err;               // sticky error bits
+  unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
+};
+
+// ----------------------------------------------------------------- addressing
+__device__ __forceinline__ char* shard_of(const DevCtx& c, int s) { return c.sym[s] + c.lay.shard; }
+__device__ __forceinline__ int* gids_of(const DevCtx& c, int s, int p, int n) {
+  return reinterpret_cast<int*>(c.sym[s] + c.lay.gids) + ((size_t)(p * c.N + n)) * c.max_tok;
+}
+__device__ __forceinline__ int* ntok_of(const DevCtx& c, int s, int p, int n) {
+  return reinterpret_cast<int*>(c.sym[s] + c.lay.ntok) + p * c.N + n;
+}
+__device__ __forceinline__ char* recv_of(const DevCtx& c, int s, int p, int n) {
+  return c.sym[s] + c.lay.recv + ((size_t)(p * c.N + n)) * c.max_tok * (size_t)c.d * c.esz;
+}
+__device__ __forceinline__ Flags* flags_of(const DevCtx& c, int s) {
+  return reinterpret_cast<Flags*>(c.sym[s] + c.lay.flags);
+}
+__device__ __forceinline__ size_t pn(const DevCtx& c, int p, int n) { return (size_t)(p * c.N + n); }
+
+// ----------------------------------------------------------------- memory model
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *flag >= target (epoch compare, wrap-safe) or the bound expires.
+__device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag, uint32_t target) {
+  if ((int)(ld_acquire_sys(flag) - target) >= 0) return;
+  unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire_sys(flag) - target) < 0) {
+    __nanosleep(64);
+    if (globaltimer() - t0 > c.timeout_ns) {
+      atomicOr(c.err, ERR_TIMEOUT);
+      return;
+    }
+  }
+}
+
+// Block-level: thread 0 waits for flag[s] >= target for every rank s, then the
+// block proceeds.  (Grids that wait are bounded to be co-resident.)
+__device__ __forceinline__ void block_wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < c.N; ++s) wait_flag(c, flags + s, target);
+  }
+  __syncthreads();
+}
+
+// Last-block pattern: every block calls this after its stores; returns true in
+// exactly one thread (thread 0 of the last block to arrive), after a system
+// fence, so it may publish flags that cover every block's stores.
+__device__ __forceinline__ bool last_block_done(unsigned int* ctr) {
+  __syncthreads();
+  bool last = false;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned int prev = atomicAdd(ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      *ctr = 0u;  // re-arm for the next launch (stream-ordered)
+      last = true;
+    }
+  }
+  return last;
+}
+
+// ----------------------------------------------------------------- vector access
+__device__ __forceinline__ uint4 ld16(const void* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ uint4 ld16_nc(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// 16 bytes -> floats (EPV = 4 for fp32, 8 for bf16)
+template <int DT>
+struct Vec;
+template <>
+struct Vec<F32> {
+  static constexpr int EPV = 4;
+  __device__ __forceinline__ static void unpack(uint4 u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t bf_pack2(float a, float b) {
+  // round-to-nearest-even to bf16 (cvt.rn.bf16x2.f32 packs hi=first operand)
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+template <>
+struct Vec<BF16> {
+  static constexpr int EPV = 8;
+  __device__ __forceinline__ static void unpack(uint4 u, float* f) {
+    f[0] = bf_lo(u.x); f[1] = bf_hi(u.x); f[2] = bf_lo(u.y); f[3] = bf_hi(u.y);
+    f[4] = bf_lo(u.z); f[5] = bf_hi(u.z); f[6] = bf_lo(u.w); f[7] = bf_hi(u.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(bf_pack2(f[0], f[1]), bf_pack2(f[2], f[3]), bf_pack2(f[4], f[5]), bf_pack2(f[6], f[7]));
+  }
+};
+
+}  // namespace emb

@@ -1,0 +1,536 @@
+// ctx.cu — C-ABI entry points (include/embrace.h): validation, library-owned
+// device state, CUDA IPC peer mapping, stream/event orchestration of the
+// exchange kernels, stats and debug access.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/embrace.h"
+#include "common.cuh"
+#include "dense_queue.h"
+#include "kernels.cuh"
+
+using namespace emb;
+
+namespace {
+
+enum CtxState { ST_CREATED = 0, ST_READY = 1, ST_AFTER_FWD = 2 };
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int bits_for(long long v) {  // bits needed to represent value v (v >= 0)
+  int b = 0;
+  while ((1ll << b) <= v) ++b;
+  return b < 1 ? 1 : b;
+}
+
+struct Plan {
+  int N, r, d, esz, cpr, cps, C, max_chunks, idbits, posbits;
+  bool key64;
+  size_t route_smem;
+  SymLayout lay;
+  size_t local_bytes;
+};
+
+emb_status make_plan(const emb_config* cfg, Plan* pl) {
+  if (!cfg) return EMB_ERR_INVALID_ARG;
+  if (cfg->world < 1 || cfg->world > EMB_MAX_WORLD) return EMB_ERR_SHAPE;
+  if (cfg->rank < 0 || cfg->rank >= cfg->world) return EMB_ERR_INVALID_ARG;
+  if (cfg->vocab < 1 || cfg->vocab >= (1ll << 30)) return EMB_ERR_INVALID_ARG;
+  if (cfg->dim < 1 || cfg->max_tokens < 1 || cfg->max_tokens > 16384) return EMB_ERR_CAPACITY;
+  if (cfg->dtype != EMB_FP32 && cfg->dtype != EMB_BF16) return EMB_ERR_INVALID_ARG;
+  if (cfg->mode < EMB_BWD_RAW || cfg->mode > EMB_BWD_SPLIT) return EMB_ERR_INVALID_ARG;
+  if (cfg->optim != EMB_SGD && cfg->optim != EMB_ADAM) return EMB_ERR_INVALID_ARG;
+  if (cfg->queue_window < 0) return EMB_ERR_INVALID_ARG;
+  const int N = cfg->world;
+  if (N > cfg->dim || cfg->dim % N != 0) return EMB_ERR_SHAPE;
+  pl->N = N;
+  pl->r = cfg->rank;
+  pl->esz = cfg->dtype == EMB_BF16 ? 2 : 4;
+  pl->d = cfg->dim / N;
+  if ((pl->d * pl->esz) % 16 != 0) return EMB_ERR_SHAPE;
+  pl->cpr = cfg->dim * pl->esz / 16;
+  pl->cps = pl->d * pl->esz / 16;
+  if (pl->cpr > 256) return EMB_ERR_SHAPE;  // rows up to 4 KB
+  pl->C = 16;
+  pl->max_chunks = cfg->max_tokens + cfg->max_tokens / pl->C + 1;
+  pl->idbits = bits_for(cfg->vocab);  // the value L itself is the invalid-id sentinel
+  pl->posbits = bits_for(cfg->max_tokens - 1);
+  pl->key64 = pl->idbits + pl->posbits > 32;
+  pl->route_smem = route_smem_bytes(cfg->max_tokens, pl->key64);
+  if (pl->route_smem > 227 * 1024) return EMB_ERR_CAPACITY;
+
+  const size_t L = (size_t)cfg->vocab, T = (size_t)cfg->max_tokens;
+  SymLayout& y = pl->lay;
+  size_t off = 0;
+  y.shard = off; off = align_up(off + L * pl->d * pl->esz, 4096);
+  y.gids = off;  off = align_up(off + 2 * N * T * 4, 4096);
+  y.ntok = off;  off = align_up(off + 2 * N * 4, 256);
+  y.recv = off;  off = align_up(off + 2 * N * T * pl->d * pl->esz, 4096);
+  y.flags = off; off = align_up(off + sizeof(Flags), 4096);
+  y.total = off;
+
+  size_t loc = 0;
+  if (cfg->optim == EMB_ADAM) loc += 2 * L * pl->d * 4;
+  loc += L * 4 + L * N * 8;
+  loc += 4 * 2 * N * T * 4 + 2 * N * (T + 1) * 4 + 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * 16;
+  loc += 2 * N * T * 4 + 2 * (size_t)pl->max_chunks * cfg->dim * 4;
+  if (cfg->mode == EMB_BWD_SPLIT) loc += 2 * T * cfg->dim * pl->esz;
+  if (cfg->mode == EMB_BWD_RAW) loc += 2 * N * T * pl->d * 4;
+  pl->local_bytes = loc;
+  return EMB_OK;
+}
+
+}  // namespace
+
+struct emb_ctx {
+  emb_config cfg;
+  Plan pl;
+  DevCtx dc;
+  LaunchCfg lc;
+  int state = ST_CREATED;
+  emb_status poisoned = EMB_OK;
+  char* sym = nullptr;
+  bool peer_open[EMB_MAX_WORLD] = {};
+  std::vector<void*> allocs;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {};
+  bool def_pending[2] = {false, false};
+  long long it = 0;          // forward calls so far (host mirror of the device t)
+  long long bwd_done = 0;
+  bool prefetched = false;   // last backward pushed next ids
+  int last_n = 0;
+  DenseQueue* dq = nullptr;
+};
+
+#define CKC(ctx, call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      fprintf(stderr, "[embrace] CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      if (ctx) (ctx)->poisoned = EMB_ERR_CUDA;                                          \
+      return EMB_ERR_CUDA;                                                              \
+    }                                                                                   \
+  } while (0)
+
+static emb_status ctx_check(emb_ctx* ctx) {
+  if (!ctx) return EMB_ERR_INVALID_ARG;
+  if (ctx->poisoned != EMB_OK) return ctx->poisoned;
+  return EMB_OK;
+}
+
+static cudaError_t dev_alloc(emb_ctx* ctx, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaSuccess) {
+    ctx->allocs.push_back(*p);
+    e = cudaMemset(*p, 0, bytes);
+  }
+  return e;
+}
+
+extern "C" {
+
+const char* emb_status_str(emb_status s) {
+  switch (s) {
+    case EMB_OK: return "EMB_OK";
+    case EMB_ERR_INVALID_ARG: return "EMB_ERR_INVALID_ARG";
+    case EMB_ERR_SHAPE: return "EMB_ERR_SHAPE";
+    case EMB_ERR_ID_RANGE: return "EMB_ERR_ID_RANGE";
+    case EMB_ERR_CAPACITY: return "EMB_ERR_CAPACITY";
+    case EMB_ERR_STATE: return "EMB_ERR_STATE";
+    case EMB_ERR_CUDA: return "EMB_ERR_CUDA";
+    case EMB_ERR_NCCL: return "EMB_ERR_NCCL";
+    case EMB_ERR_TIMEOUT: return "EMB_ERR_TIMEOUT";
+  }
+  return "EMB_ERR_UNKNOWN";
+}
+
+emb_status emb_workspace_bytes(const emb_config* cfg, size_t* symmetric_bytes, size_t* local_bytes) {
+  Plan pl;
+  emb_status st = make_plan(cfg, &pl);
+  if (st != EMB_OK) return st;
+  if (symmetric_bytes) *symmetric_bytes = pl.lay.total;
+  if (local_bytes) *local_bytes = pl.local_bytes;
+  return EMB_OK;
+}
+
+emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
+  if (!out) return EMB_ERR_INVALID_ARG;
+  *out = nullptr;
+  Plan pl;
+  emb_status st = make_plan(cfg, &pl);
+  if (st != EMB_OK) return st;
+  emb_ctx* ctx = new (std::nothrow) emb_ctx();
+  if (!ctx) return EMB_ERR_CUDA;
+  ctx->cfg = *cfg;
+  if (ctx->cfg.queue_window < 1) ctx->cfg.queue_window = 1;
+  ctx->pl = pl;
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) { delete ctx; return EMB_ERR_CUDA; }
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  ctx->lc.nsm = nsm > 0 ? nsm : 148;
+
+  DevCtx& c = ctx->dc;
+  memset(&c, 0, sizeof(c));
+  c.N = pl.N; c.r = pl.r; c.L = cfg->vocab; c.D = cfg->dim; c.d = pl.d; c.esz = pl.esz;
+  c.dtype = cfg->dtype == EMB_BF16 ? BF16 : F32;
+  c.mode = (int)cfg->mode; c.optim = cfg->optim == EMB_ADAM ? ADAM : SGD;
+  c.max_tok = cfg->max_tokens; c.cpr = pl.cpr; c.cps = pl.cps; c.pad_id = cfg->pad_id;
+  c.lr = cfg->lr; c.beta1 = cfg->beta1; c.beta2 = cfg->beta2; c.eps = cfg->eps;
+  c.scale = cfg->grad_scale != 0.f ? cfg->grad_scale : 1.0f / (float)pl.N;
+  c.timeout_ns = (unsigned long long)(cfg->timeout_ms > 0 ? cfg->timeout_ms : 10000) * 1000000ull;
+  c.C = pl.C; c.max_chunks = pl.max_chunks; c.idbits = pl.idbits; c.posbits = pl.posbits;
+  c.lay = pl.lay;
+
+#define ALLOC(ptr, bytes) \
+  do { void* p_ = nullptr; if (dev_alloc(ctx, &p_, (bytes)) != cudaSuccess) goto fail; ptr = reinterpret_cast<decltype(ptr)>(p_); } while (0)
+  {
+    const size_t L = (size_t)cfg->vocab, T = (size_t)cfg->max_tokens, N = pl.N;
+    // symmetric region: plain cudaMalloc so it can be IPC-exported
+    if (cudaMalloc(reinterpret_cast<void**>(&ctx->sym), pl.lay.total) != cudaSuccess) goto fail;
+    // zero ids/ntok/flags now: peers may write into them as soon as handles are exchanged
+    if (cudaMemset(ctx->sym + pl.lay.gids, 0, pl.lay.recv - pl.lay.gids) != cudaSuccess) goto fail;
+    if (cudaMemset(ctx->sym + pl.lay.flags, 0, sizeof(Flags)) != cudaSuccess) goto fail;
+    c.sym[pl.r] = ctx->sym;
+    if (cfg->optim == EMB_ADAM) {
+      ALLOC(c.adam_m, L * pl.d * 4);
+      ALLOC(c.adam_v, L * pl.d * 4);
+    }
+    ALLOC(c.nextmark, L * 4);
+    ALLOC(c.slotmap, L * N * 8);
+    ALLOC(c.perm, 2 * N * T * 4);
+    ALLOC(c.slot_id, 2 * N * T * 4);
+    ALLOC(c.seg_start, 2 * N * T * 4);
+    ALLOC(c.seg_end, 2 * N * T * 4);
+    ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
+    ALLOC(c.chunk_slot, 2 * N * (size_t)pl.max_chunks * 4);
+    ALLOC(c.counts, 2 * N * 4 * 4);
+    ALLOC(c.slot_ctr, 2 * N * T * 4);
+    ALLOC(c.scratch, 2 * (size_t)pl.max_chunks * cfg->dim * 4);
+    if (cfg->mode == EMB_BWD_SPLIT) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
+    if (cfg->mode == EMB_BWD_RAW) ALLOC(c.gc_owner, 2 * N * T * pl.d * 4);
+    ALLOC(c.done_ctr, 32 * 4);
+    ALLOC(c.t_rec, 2 * 4);
+    ALLOC(c.err, 4);
+    ALLOC(c.stats, 3 * N * 8);
+  }
+#undef ALLOC
+  if (route_set_smem(pl.key64, pl.route_smem) != cudaSuccess) goto fail;
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
+    if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo) != cudaSuccess) goto fail;
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (cudaEventCreateWithFlags(&ctx->ev_prior[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+    if (cudaEventCreateWithFlags(&ctx->ev_def[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
+  *out = ctx;
+  return EMB_OK;
+fail:
+  fprintf(stderr, "[embrace] emb_create failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->sym) cudaFree(ctx->sym);
+  delete ctx;
+  return EMB_ERR_CUDA;
+}
+
+emb_status emb_ipc_handle(emb_ctx* ctx, uint8_t* handle_out) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!handle_out) return EMB_ERR_INVALID_ARG;
+  static_assert(sizeof(cudaIpcMemHandle_t) == EMB_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  CKC(ctx, cudaIpcGetMemHandle(&h, ctx->sym));
+  memcpy(handle_out, &h, sizeof(h));
+  return EMB_OK;
+}
+
+emb_status emb_get_unique_id(uint8_t* id_out) {
+  if (!id_out) return EMB_ERR_INVALID_ARG;
+  static_assert(sizeof(ncclUniqueId) == EMB_UNIQUE_ID_BYTES, "nccl id size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return EMB_ERR_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return EMB_OK;
+}
+
+// boot barrier over the flags region: every rank stores 1 into every peer's
+// boot slot after its shard copy, then waits for all (bounded).
+__global__ void boot_kernel(DevCtx c, uint32_t val) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int s = 0; s < c.N; ++s) st_release_sys(&flags_of(c, s)->boot[c.r], val);
+  for (int s = 0; s < c.N; ++s) wait_flag(c, &flags_of(c, c.r)->boot[s], val);
+}
+
+emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8_t* nccl_id,
+                          const void* shard_init, emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (ctx->state != ST_CREATED) return EMB_ERR_STATE;
+  if (!shard_init || (ctx->pl.N > 1 && !peer_handles)) return EMB_ERR_INVALID_ARG;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  for (int s = 0; s < ctx->pl.N; ++s) {
+    if (s == ctx->pl.r) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, peer_handles + (size_t)s * EMB_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    CKC(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->dc.sym[s] = static_cast<char*>(p);
+    ctx->peer_open[s] = true;
+  }
+  const size_t shard_bytes = (size_t)ctx->cfg.vocab * ctx->pl.d * ctx->pl.esz;
+  CKC(ctx, cudaMemcpyAsync(ctx->sym + ctx->pl.lay.shard, shard_init, shard_bytes, cudaMemcpyDeviceToDevice, stream));
+  if (ctx->dc.adam_m) {
+    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_m, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
+    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_v, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
+  }
+  boot_kernel<<<1, 32, 0, stream>>>(ctx->dc, 1u);
+  CKC(ctx, cudaGetLastError());
+  CKC(ctx, cudaStreamSynchronize(stream));
+  int err = 0;
+  CKC(ctx, cudaMemcpy(&err, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
+  if (err & ERR_TIMEOUT) { ctx->poisoned = EMB_ERR_TIMEOUT; return EMB_ERR_TIMEOUT; }
+  if (nccl_id) {
+    ctx->dq = dense_queue_create(nccl_id, ctx->pl.N, ctx->pl.r, ctx->cfg.queue_window);
+    if (!ctx->dq) { ctx->poisoned = EMB_ERR_NCCL; return EMB_ERR_NCCL; }
+  }
+  ctx->state = ST_READY;
+  return EMB_OK;
+}
+
+emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, void* out, emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (ctx->state == ST_CREATED) return EMB_ERR_STATE;
+  if (n < 0 || n > ctx->cfg.max_tokens) return EMB_ERR_CAPACITY;
+  if (n > 0 && (!ids || !out)) return EMB_ERR_INVALID_ARG;
+  if (ctx->state == ST_AFTER_FWD) return EMB_ERR_STATE;  // backward of the previous forward missing
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  ctx->it += 1;
+  const int p = (int)(ctx->it & 1);
+  if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+  CKC(ctx, launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, ctx->prefetched ? 1 : 0, stream));
+  ctx->prefetched = false;
+  ctx->last_n = n;
+  ctx->state = ST_AFTER_FWD;
+  return EMB_OK;
+}
+
+emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32_t* next_ids, int32_t n_next,
+                                 emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (ctx->state != ST_AFTER_FWD) return EMB_ERR_STATE;
+  if (ctx->last_n > 0 && !grad_out) return EMB_ERR_INVALID_ARG;
+  if (next_ids && (n_next < 0 || n_next > ctx->cfg.max_tokens)) return EMB_ERR_CAPACITY;
+  if (!next_ids) n_next = 0;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const int p = (int)(ctx->it & 1);
+  const DevCtx& c = ctx->dc;
+  const int mode = ctx->cfg.mode;
+  CKC(ctx, launch_ids(c, ctx->lc, next_ids, n_next, p, (mode == EMB_BWD_SPLIT && next_ids) ? 1 : 0, stream));
+  CKC(ctx, launch_route(c, ctx->lc, p, ctx->pl.key64, ctx->pl.route_smem, stream));
+  if (mode == EMB_BWD_RAW) {
+    CKC(ctx, launch_rawpush(c, ctx->lc, grad_out, ctx->last_n, p, stream));
+    CKC(ctx, launch_rawcoal(c, ctx->lc, p, stream));
+    CKC(ctx, launch_merge(c, ctx->lc, p, 0, stream));
+  } else {
+    CKC(ctx, launch_coal(c, ctx->lc, grad_out, p, stream));
+    CKC(ctx, launch_merge(c, ctx->lc, p, 0, stream));
+    if (mode == EMB_BWD_SPLIT) {
+      // scheduled part: lowest-priority side stream, after the prior part
+      CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));
+      CKC(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_prior[p], 0));
+      CKC(ctx, launch_defpush(c, ctx->lc, p, ctx->side));
+      CKC(ctx, launch_merge(c, ctx->lc, p, 1, ctx->side));
+      CKC(ctx, cudaEventRecord(ctx->ev_def[p], ctx->side));
+      ctx->def_pending[p] = true;
+    }
+  }
+  ctx->prefetched = next_ids != nullptr;
+  ctx->bwd_done += 1;
+  ctx->state = ST_READY;
+  return EMB_OK;
+}
+
+emb_status dense_allreduce_enqueue(emb_ctx* ctx, void* buf, int64_t count, emb_dtype dtype, int32_t priority,
+                                   emb_event_t ready, int64_t* ticket) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!ctx->dq) return EMB_ERR_STATE;
+  if (!buf || count < 0 || !ticket || (dtype != EMB_FP32 && dtype != EMB_BF16)) return EMB_ERR_INVALID_ARG;
+  st = dense_queue_enqueue(ctx->dq, buf, count, dtype, priority, reinterpret_cast<cudaEvent_t>(ready), ticket);
+  if (st == EMB_ERR_CUDA || st == EMB_ERR_NCCL) ctx->poisoned = st;
+  return st;
+}
+
+emb_status dense_queue_flush(emb_ctx* ctx) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!ctx->dq) return EMB_OK;
+  st = dense_queue_flush_all(ctx->dq);
+  if (st == EMB_ERR_CUDA || st == EMB_ERR_NCCL) ctx->poisoned = st;
+  return st;
+}
+
+emb_status dense_wait(emb_ctx* ctx, int64_t ticket, emb_stream_t consumer) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!ctx->dq) return EMB_ERR_STATE;
+  return dense_queue_wait(ctx->dq, ticket, reinterpret_cast<cudaStream_t>(consumer));
+}
+
+static emb_status sticky_err(emb_ctx* ctx) {
+  int err = 0;
+  CKC(ctx, cudaMemcpy(&err, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
+  if (err & ERR_ID) return EMB_ERR_ID_RANGE;
+  if (err & ERR_STATE) return EMB_ERR_STATE;
+  if (err & ERR_TIMEOUT) return EMB_ERR_TIMEOUT;
+  return EMB_OK;
+}
+
+emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  for (int p = 0; p < 2; ++p)
+    if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+  if (ctx->dq) {
+    st = dense_queue_flush_all(ctx->dq);
+    if (st != EMB_OK) { ctx->poisoned = st; return st; }
+    st = dense_queue_wait_all(ctx->dq, stream);
+    if (st != EMB_OK) { ctx->poisoned = st; return st; }
+  }
+  CKC(ctx, cudaStreamSynchronize(stream));
+  return sticky_err(ctx);
+}
+
+emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!out) return EMB_ERR_INVALID_ARG;
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  CKC(ctx, cudaDeviceSynchronize());
+  memset(out, 0, sizeof(*out));
+  const int N = ctx->pl.N;
+  out->iter = ctx->bwd_done;
+  out->world = N;
+  if (ctx->bwd_done > 0) {
+    const int p = (int)(ctx->it & 1);
+    std::vector<int> cnt(N * 4);
+    CKC(ctx, cudaMemcpy(cnt.data(), ctx->dc.counts + (size_t)p * N * 4, N * 16, cudaMemcpyDeviceToHost));
+    for (int n = 0; n < N; ++n) {
+      out->n_tokens[n] = cnt[n * 4 + 0];
+      out->u[n] = cnt[n * 4 + 1];
+      out->p[n] = cnt[n * 4 + 2];
+      out->q[n] = cnt[n * 4 + 1] - cnt[n * 4 + 2];
+    }
+  }
+  std::vector<unsigned long long> s(3 * N);
+  CKC(ctx, cudaMemcpy(s.data(), ctx->dc.stats, 3 * N * 8, cudaMemcpyDeviceToHost));
+  for (int n = 0; n < N; ++n) {
+    out->fwd_bytes_pulled[n] = (int64_t)s[n];
+    out->bwd_bytes_pushed[n] = (int64_t)s[N + n];
+    out->ids_bytes_pushed[n] = (int64_t)s[2 * N + n];
+  }
+  CKC(ctx, cudaMemcpy(&out->err_flags, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
+  return EMB_OK;
+}
+
+emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, size_t cap, size_t* n) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!n || (!host && cap)) return EMB_ERR_INVALID_ARG;
+  const int N = ctx->pl.N;
+  *n = 0;
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  CKC(ctx, cudaDeviceSynchronize());
+  if (item == EMB_DBG_ISSUE_LOG) {
+    std::vector<int64_t> log;
+    if (ctx->dq) dense_queue_issue_log(ctx->dq, &log);
+    *n = log.size();
+    if (cap < log.size() * 8) return EMB_ERR_CAPACITY;
+    if (!log.empty()) memcpy(host, log.data(), log.size() * 8);
+    return EMB_OK;
+  }
+  if (ctx->bwd_done == 0) return EMB_ERR_STATE;
+  const int p = (int)(ctx->it & 1);
+  if (item == EMB_DBG_COUNTS) {
+    *n = (size_t)N * 4;
+    if (cap < *n * 4) return EMB_ERR_CAPACITY;
+    CKC(ctx, cudaMemcpy(host, ctx->dc.counts + (size_t)p * N * 4, N * 16, cudaMemcpyDeviceToHost));
+    return EMB_OK;
+  }
+  if (src < 0 || src >= N) return EMB_ERR_INVALID_ARG;
+  int cnt[4];
+  CKC(ctx, cudaMemcpy(cnt, ctx->dc.counts + ((size_t)p * N + src) * 4, 16, cudaMemcpyDeviceToHost));
+  const int* dptr = nullptr;
+  size_t len = 0;
+  const size_t off = ((size_t)p * N + src) * ctx->cfg.max_tokens;
+  switch (item) {
+    case EMB_DBG_GIDS:
+      dptr = reinterpret_cast<const int*>(ctx->sym + ctx->pl.lay.gids) + off;
+      len = cnt[0];
+      break;
+    case EMB_DBG_SLOT_IDS: dptr = ctx->dc.slot_id + off; len = cnt[1]; break;
+    case EMB_DBG_PERM: dptr = ctx->dc.perm + off; len = cnt[0]; break;
+    default: return EMB_ERR_INVALID_ARG;
+  }
+  *n = len;
+  if (cap < len * 4) return EMB_ERR_CAPACITY;
+  if (len) CKC(ctx, cudaMemcpy(host, dptr, len * 4, cudaMemcpyDeviceToHost));
+  return EMB_OK;
+}
+
+emb_status emb_state_ptr(emb_ctx* ctx, int32_t item, void** ptr) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!ptr) return EMB_ERR_INVALID_ARG;
+  switch (item) {
+    case EMB_STATE_SHARD: *ptr = ctx->sym + ctx->pl.lay.shard; return EMB_OK;
+    case EMB_STATE_ADAM_M: *ptr = ctx->dc.adam_m; return ctx->dc.adam_m ? EMB_OK : EMB_ERR_STATE;
+    case EMB_STATE_ADAM_V: *ptr = ctx->dc.adam_v; return ctx->dc.adam_v ? EMB_OK : EMB_ERR_STATE;
+  }
+  return EMB_ERR_INVALID_ARG;
+}
+
+emb_status emb_queue_issue_order(const int32_t* priorities, int32_t n, int32_t window, int32_t* out) {
+  if (n < 0 || window < 1 || (n > 0 && (!priorities || !out))) return EMB_ERR_INVALID_ARG;
+  std::vector<int64_t> order;
+  issue_rule_order(priorities, n, window, &order);
+  for (int i = 0; i < n; ++i) out[i] = (int32_t)order[i];
+  return EMB_OK;
+}
+
+emb_status emb_shard_destroy(emb_ctx* ctx) {
+  if (!ctx) return EMB_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  if (ctx->dq) dense_queue_destroy(ctx->dq);
+  for (int s = 0; s < EMB_MAX_WORLD; ++s)
+    if (ctx->peer_open[s]) cudaIpcCloseMemHandle(ctx->dc.sym[s]);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->sym) cudaFree(ctx->sym);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_prior[i]) cudaEventDestroy(ctx->ev_prior[i]);
+    if (ctx->ev_def[i]) cudaEventDestroy(ctx->ev_def[i]);
+  }
+  delete ctx;
+  return EMB_OK;
+}
+
+}  // extern "C"
