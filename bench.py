@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""bench.py — EmbRace sparse-embedding fwd+bwd exchange throughput on B200.
+
+One step = emb_forward_exchange + emb_backward_exchange of one synthetic batch
+per rank (all of SURVEY §8(a): id all-gather, pull-gather forward, next-id
+prefetch + D_next marks, per-source sort/unique/split, sender coalesce + push,
+owner merge + fused optimizer update, scheduled part on the side stream).  The
+timed region ends after every deferred (scheduled) update has completed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config lstm_lm]
+                  [--mode split] [--impl ours|reference] [--no-graph]
+
+N > 1 runs under torchrun (one process per GPU).  Default workload:
+BASELINE.json configs[1] (LSTM-LM 793,470 x 512 fp32, 128 x 35 Zipf batches per
+rank, SPLIT mode, Adam) — the configuration the metric is quoted on; it fits
+one GPU.  Prints ONE JSON line on rank 0.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synthetic import get_config  # noqa: E402
+from synthetic.workloads import PAD_ID, gen_dY, gen_ids, gen_table  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+METRIC = "sparse embedding fwd+bwd exchange tokens/s at 1/2/4/8 B200; % HBM/NVLink roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="lstm_lm")
+    ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=64)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------- clocks (NVML, sampled in a thread)
+class ClockSampler:
+    def __init__(self, device_index, period_s=0.002):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- workload
+def n_batches(cfg, N):
+    """Enough distinct batches that the inputs+outputs cycled through exceed
+    2x L2 (126 MB) between reuse (timing rule: inputs larger than L2)."""
+    esz = 2 if cfg.dtype == "bf16" else 4
+    per = 2 * cfg.max_tokens * cfg.D * esz           # dY read + Y written per batch
+    nb = int(np.ceil(2 * L2_BYTES / per))
+    nb += nb % 2                                     # even: graph replays keep the parity
+    return max(4, min(nb, 64))
+
+
+def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
+    """Per-kernel algorithmic bytes of one step on `rank`,
+    from the actual ids.  Returns {kernel: (hbm_bytes, nvlink_bytes)}."""
+    esz = 2 if cfg.dtype == "bf16" else 4
+    d = cfg.D // N
+    T = [len(x) for x in ids_all]
+    ids_r = np.asarray(ids_all[rank])
+    u_fwd = len(np.unique(ids_r))
+    U_n = [np.unique(x) for x in ids_all]
+    u = [len(x) for x in U_n]
+    Uall = np.unique(np.concatenate(ids_all))
+    nxt = np.unique(np.concatenate(next_all))
+    P = np.intersect1d(Uall, nxt).size if mode == "split" else Uall.size
+    Q = Uall.size - P
+    out = {}
+    # forward: Y write + distinct rows read (every owner's slice) + ids; NVLink in = (N-1)/N of rows
+    out["fwd_pull_gather"] = (T[rank] * cfg.D * esz + u_fwd * cfg.D * esz + T[rank] * 4,
+                              (N - 1) * T[rank] * d * esz)
+    out["ids_push_mark"] = (sum(T) * 4 + T[rank] * 4 * N + (sum(T) * 4 if mode == "split" else 0),
+                            (N - 1) * T[rank] * 4)
+    out["route_sort_split"] = (sum(T) * 4 * 2 + sum(u) * 4 * 4 + sum(u) * 8, 0)
+    c_r = T[rank] if mode == "raw" else u[rank]
+    if mode == "raw":
+        out["rawpush"] = (T[rank] * cfg.D * esz * 2, (N - 1) * T[rank] * d * esz)
+        out["rawcoal"] = (sum(T) * d * esz + sum(u) * d * 4, 0)
+        src = 4
+    else:
+        out["coal_push"] = (T[rank] * cfg.D * esz + c_r * cfg.D * esz, (N - 1) * c_r * d * esz)
+        src = esz
+    opt_b = 16 if cfg.optim == "adam" else 0
+    frac_p = (P / Uall.size) if Uall.size else 0
+    contrib = sum(u) * d * src
+    out["merge_update_prior"] = (int(frac_p * contrib) + P * d * (2 * esz + opt_b), 0)
+    if mode == "split":
+        q_r = len(np.setdiff1d(U_n[rank], nxt))
+        out["defpush"] = (2 * q_r * cfg.D * esz, (N - 1) * q_r * d * esz)
+        out["merge_update_sched"] = (int((1 - frac_p) * contrib) + Q * d * (2 * esz + opt_b), 0)
+    return out
+
+
+def make_batches(cfg, N, rank, nb):
+    ids = [gen_ids(cfg, b, rank) for b in range(nb)]
+    ids_all = [[gen_ids(cfg, b, s) for s in range(N)] for b in range(nb)] if N > 1 else [[x] for x in ids]
+    dY = [gen_dY(cfg, b, rank, len(ids[b])) for b in range(nb)]
+    return ids, ids_all, dY
+
+
+# ---------------------------------------------------------------- oracle timing (CPU baseline / reference arm)
+def oracle_step_fn(cfg, N, mode, budget_s):
+    """Returns (step(k) -> tokens processed, sample description).  The oracle
+    simulates all N workers of one iteration of the same workload; if a full
+    iteration exceeds `budget_s`, each step runs on the first B' sequences of
+    every rank (a bounded sample) and counts only those tokens."""
+    from oracle import exchange, partition
+    opt = exchange.OptimConfig(cfg.optim, lr=cfg.lr)
+    W = gen_table(cfg)
+    shards = partition.partition_columnwise(W, N)
+    del W
+    m = [np.zeros_like(s) for s in shards] if cfg.optim == "adam" else None
+    v = [np.zeros_like(s) for s in shards] if cfg.optim == "adam" else None
+    nb = 4
+    ids = [[gen_ids(cfg, b, s) for s in range(N)] for b in range(nb)]
+    dY = [[gen_dY(cfg, b, s, len(ids[b][s])) for s in range(N)] for b in range(nb)]
+    state = {"t": 0, "frac": 1.0}
+
+    def run(k, frac):
+        b = k % nb
+        cut = [max(1, int(len(x) * frac)) for x in ids[b]]
+        I = [ids[b][s][: cut[s]] for s in range(N)]
+        G = [dY[b][s][: cut[s]] for s in range(N)]
+        nxt = [ids[(b + 1) % nb][s][: cut[s]] for s in range(N)]
+        state["t"] += 1
+        exchange.simulate_iteration(shards, I, G, nxt, state["t"], mode, cfg.dtype, opt, m, v)
+        return sum(int((x != PAD_ID).sum()) for x in I)
+
+    t0 = time.perf_counter()
+    run(0, 1.0)
+    full = time.perf_counter() - t0
+    if full > budget_s:
+        state["frac"] = max(0.02, budget_s / full)
+    frac = state["frac"]
+    desc = (f"oracle.exchange.simulate_iteration, {N} simulated worker(s), mode {mode}; "
+            + ("full iterations" if frac >= 1.0 else f"first {frac:.1%} of every rank's batch per step"))
+    return (lambda k: run(k, frac)), desc
+
+
+def cpu_baseline(cfg, N, mode, seconds=12.0):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    step, desc = oracle_step_fn(cfg, N, mode, budget_s=seconds / 3)
+    toks, k = 0, 1
+    t0 = time.perf_counter()
+    while True:
+        toks += step(k)
+        k += 1
+        el = time.perf_counter() - t0
+        if el > seconds or k > 200:
+            break
+    return {"value": toks / el, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{desc}; {k - 1} timed steps in {el:.1f} s (single-threaded NumPy)"}
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    step, desc = oracle_step_fn(cfg, world, args.mode, budget_s=1.0)
+    for k in range(args.warmup):
+        step(k)
+    toks = 0
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        toks += step(args.warmup + k)
+    el = time.perf_counter() - t0
+    val = toks / el
+    line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} (oracle on host cores)", "mode": args.mode, "ranks": world},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        world = args.gpus if world == 1 else world
+    cfg = get_config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2110_09132_b200 import embrace as E
+    from paper_2110_09132_b200.runtime import EmbraceExchange
+
+    mode = args.mode
+    nb = n_batches(cfg, world)
+    ids, ids_all, dY = make_batches(cfg, world, rank, nb)
+    ids_d = [torch.from_numpy(x).to(dev) for x in ids]
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    dY_d = [torch.from_numpy(x).to(dev).to(tdt) for x in dY]
+    Y_d = [torch.empty((len(x), cfg.D), dtype=tdt, device=dev) for x in ids]
+    d = cfg.D // world
+    W = gen_table(cfg)
+    shard0 = torch.from_numpy(np.ascontiguousarray(W[:, rank * d:(rank + 1) * d])).to(dev).to(tdt)
+    del W
+    ex = EmbraceExchange(cfg.L, cfg.D, shard0, world=world, rank=rank, device=local, dtype=cfg.dtype,
+                         max_tokens=cfg.max_tokens, mode=mode, optim=cfg.optim, lr=cfg.lr)
+    del shard0
+    stream = torch.cuda.current_stream()
+
+    def step(k):
+        b = k % nb
+        E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], stream)
+        E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    E.emb_join(ex.ctx, stream)
+    torch.cuda.synchronize()
+
+    # CUDA graph of one full cycle of nb steps (device-resident iteration counter -> replay-safe)
+    graph = None
+    k0 = args.warmup
+    if not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            cap_stream = torch.cuda.Stream()
+            cap_stream.wait_stream(stream)
+            with torch.cuda.graph(g, stream=cap_stream):
+                for j in range(nb):
+                    b = (k0 + j) % nb
+                    E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], cap_stream)
+                    E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], cap_stream)
+                E.emb_join(ex.ctx, cap_stream)
+            stream.wait_stream(cap_stream)
+            graph = g
+            torch.cuda.synchronize()
+            graph.replay()          # one untimed replay (it is also a warm-up cycle)
+            torch.cuda.synchronize()
+        except Exception as e:  # pragma: no cover
+            print(f"[bench] graph capture failed, timing eagerly: {e}", file=sys.stderr)
+            graph = None
+
+    # ---------------- timed region
+    K = args.steps
+    n_rep, rem = (divmod(K, nb) if graph is not None else (0, K))
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(n_rep):
+            graph.replay()
+        for j in range(rem):
+            step(k0 + j)
+        E.emb_join(ex.ctx, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    kk = k0 + rem                  # next batch index (graph replays are whole cycles)
+    t_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    nonpad = sum(int((np.asarray(ids_all[(k0 + j) % nb][s]) != PAD_ID).sum())
+                 for j in range(K) for s in range(world))   # cycles are whole, so batch order is irrelevant
+    value = nonpad / (t_max / 1e3)
+
+    # ---------------- per-kernel CUDA-event profile (separate, eager, not part of `value`)
+    E.emb_profile(ex.ctx, True)
+    P = args.profile_steps
+    for j in range(P):
+        step(kk + j)
+    E.emb_join(ex.ctx, stream)
+    prof = E.emb_profile_read(ex.ctx)
+    E.emb_profile(ex.ctx, False)
+    # kernels per step: count the profiled launches (one step = one fwd + one bwd)
+    per_step_launch = sum(c for (_, c) in prof.values()) / P
+    k_prof = kk
+    kk += P
+
+    # algorithmic bytes per kernel, averaged over the profiled batches
+    alg = {}
+    for j in range(P):
+        b = (k_prof + j) % nb
+        for kname, (hb, nv) in algorithmic_bytes(cfg, world, rank, ids_all[b], ids_all[(b + 1) % nb],
+                                                 mode).items():
+            a = alg.setdefault(kname, [0, 0])
+            a[0] += hb / P
+            a[1] += nv / P
+    kern = {}
+    for kname, (tot_ms, cnt) in prof.items():
+        avg_us = tot_ms / cnt * 1e3
+        hb, nv = alg.get(kname, (0, 0))
+        kern[kname] = {"avg_us": round(avg_us, 3), "launches": cnt, "hbm_bytes": int(hb), "nvlink_bytes": int(nv),
+                       "hbm_gbs": round(hb / (avg_us * 1e-6) / 1e9, 1) if avg_us > 0 else None}
+    dom = max(kern, key=lambda k: kern[k]["avg_us"])
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    nvl_peak = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
+    dk = kern[dom]
+    nvl_gbs = dk["nvlink_bytes"] / (dk["avg_us"] * 1e-6) / 1e9 if dk["avg_us"] > 0 else 0
+    hbm_gbs = dk["hbm_gbs"] or 0
+    bound = "hbm" if (hbm_gbs / hbm_peak) >= (nvl_gbs / nvl_peak) or world == 1 else "nvlink"
+    roof = {"bound": bound, "kernel": dom,
+            "achieved": round(hbm_gbs if bound == "hbm" else nvl_gbs, 1),
+            "peak": hbm_peak if bound == "hbm" else nvl_peak, "unit": "GB/s",
+            "frac": round((hbm_gbs / hbm_peak) if bound == "hbm" else (nvl_gbs / nvl_peak), 4),
+            "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if bound == "hbm" else
+            "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
+
+    # whole-step roofline (t_roof / t_measured), SURVEY §8(d)
+    step_hbm = sum(v[0] for v in alg.values())
+    step_nvl = sum(v[1] for v in alg.values())
+    t_roof_us = max(step_hbm / (hbm_peak * 1e9), step_nvl / (nvl_peak * 1e9) if world > 1 else 0) * 1e6
+    ms_per_step = t_max / K
+
+    # ---------------- end to end through the C ABI with host buffers (pinned)
+    Ke = min(K, 200)
+    h_ids = [x.cpu().pin_memory() for x in ids_d]
+    h_dY = [x.cpu().pin_memory() for x in dY_d]
+    h_Y = [torch.empty(y.shape, dtype=y.dtype).pin_memory() for y in Y_d]
+    h2d = d2h = 0
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the next-ids buffer of step k is the ids buffer of step k+1 (prefetch contract)
+    ids_buf = [torch.empty(cfg.max_tokens, dtype=torch.int32, device=dev) for _ in range(3)]
+    dY_buf = torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev)
+    Y_buf = torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev)
+    e0.record(stream)
+    for j in range(Ke):
+        b = (kk + j) % nb
+        bn = (b + 1) % nb
+        n, nn = h_ids[b].numel(), h_ids[bn].numel()
+        cur, nxt = ids_buf[j % 3][:n], ids_buf[(j + 1) % 3][:nn]
+        if j == 0:
+            cur.copy_(h_ids[b], non_blocking=True)
+            h2d += n * 4
+        nxt.copy_(h_ids[bn], non_blocking=True)
+        dY_buf[:n].copy_(h_dY[b], non_blocking=True)
+        h2d += nn * 4 + h_dY[b].numel() * h_dY[b].element_size()
+        E.emb_forward_exchange(ex.ctx, cur, Y_buf[:n], stream)
+        E.emb_backward_exchange(ex.ctx, dY_buf[:n], nxt, stream)
+        h_Y[b].copy_(Y_buf[:n], non_blocking=True)
+        d2h += h_Y[b].numel() * h_Y[b].element_size()
+    E.emb_join(ex.ctx, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_tok = sum(int((np.asarray(ids_all[(kk + j) % nb][s]) != PAD_ID).sum()) for j in range(Ke) for s in range(world))
+    ex.flush()
+    err = ex.stats()["err_flags"]
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, 1, mode)
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: L={cfg.L} D={cfg.D} {cfg.dtype} table, "
+                                   + (f"packed <= {cfg.seq_len} tokens" if cfg.packed else
+                                      f"{cfg.batch}x{cfg.seq_len} Zipf({cfg.zipf_s}) ids") + " per rank",
+                       "mode": mode, "optim": cfg.optim, "parallelism": f"column-shard x{world}",
+                       "batches_cycled": nb, "l2": f"rotating {nb} batches (inputs+outputs "
+                       f"{nb * 2 * cfg.max_tokens * cfg.D * (2 if cfg.dtype == 'bf16' else 4) / 2**20:.0f} MiB > 126 MiB L2)",
+                       "cuda_graph": graph is not None, "tokens_counted": "non-pad (id 0 = pad)"},
+            "roofline": roof,
+            "step_roofline": {"t_roof_us": round(t_roof_us, 3), "t_step_us": round(ms_per_step * 1e3, 3),
+                              "frac": round(t_roof_us / (ms_per_step * 1e3), 4),
+                              "hbm_bytes": int(step_hbm), "nvlink_bytes": int(step_nvl)},
+            "kernels": kern,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(h2d / Ke), "d2h_bytes_per_step": int(d2h / Ke),
+                    "steps": Ke, "path": "pinned host ids/dY -> H2D -> emb_forward/backward_exchange -> Y D2H"},
+            "gpu_launches": int(round(per_step_launch * K)),
+            "gpu_launches_per_step": per_step_launch,
+            "clocks": clk.summary(),
+            "device_errors": err,
+        }
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -105,7 +105,22 @@ typedef struct {
   int64_t bwd_bytes_pushed[EMB_MAX_WORLD]; /* gradient slices written to owner s     */
   int64_t ids_bytes_pushed[EMB_MAX_WORLD]; /* token ids written to peer s            */
   int32_t err_flags;                     /* sticky device flags: 1 id range, 2 state, 4 timeout */
+  int64_t kernel_launches;               /* cumulative kernels this context launched            */
 } emb_stats;
+
+/* Kernel kinds for the optional per-kernel CUDA-event profile.              */
+typedef enum {
+  EMB_K_FWD = 0,      /* a1-a4 forward pull-gather (+ id all-gather push)        */
+  EMB_K_SORT = 1,     /* a6 per-source sort / unique (auxiliary stream)           */
+  EMB_K_ROUTE = 2,    /* a5 + a8 next-id push, D_next, Alg. 1 split, chunks       */
+  EMB_K_COAL = 3,     /* a7 + a9 + a10 sender coalesce + prior push               */
+  EMB_K_MERGE0 = 4,   /* a11 owner merge + update, prior (or whole) part          */
+  EMB_K_DEFPUSH = 5,  /* a12 scheduled rows push                                  */
+  EMB_K_MERGE1 = 6,   /* a12 owner merge + update, scheduled part                 */
+  EMB_K_RAWPUSH = 7,  /* RAW a10 raw slice push                                   */
+  EMB_K_RAWCOAL = 8,  /* RAW owner-side coalesce                                  */
+  EMB_NUM_KERNELS = 9
+} emb_kernel_kind;
 
 /* Debug items for emb_debug_copy (integer parity tests). `src` selects the
  * source rank n where it applies.  All copies are synchronous.              */
@@ -114,8 +129,10 @@ typedef enum {
   EMB_DBG_SLOT_IDS = 1, /* int32 [u_src]  source src's unique grad ids in slot order:
                            prior part ascending, then scheduled part ascending      */
   EMB_DBG_COUNTS = 2,   /* int32 [4*N]    per source: T, u, p, nchunks               */
-  EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src stably sorted by id */
-  EMB_DBG_ISSUE_LOG = 4 /* int64 [k]      dense-queue tickets in issue order          */
+  EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src sorted by (dropped, id,
+                           position); slot k's rows are perm[seg_start[k] .. seg_end[k]) */
+  EMB_DBG_ISSUE_LOG = 4, /* int64 [k]     dense-queue tickets in issue order          */
+  EMB_DBG_TIMESTAMPS = 5  /* uint64 [64]   device phase timestamps (EMB_PHASE_TIMING builds) */
 } emb_debug_item;
 
 typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1, EMB_STATE_ADAM_V = 2 } emb_state_item;
@@ -195,6 +212,18 @@ emb_status dense_wait(emb_ctx* ctx, int64_t ticket, emb_stream_t consumer);
  * the dense queue, then synchronise it; returns the sticky device error as a
  * status (EMB_ERR_ID_RANGE / STATE / TIMEOUT) if one was raised.           */
 emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream);
+
+/* Make `stream` wait (no host synchronisation) for all outstanding deferred
+ * work, so that work enqueued on it afterwards — or an event recorded on it —
+ * follows every update of every iteration so far.                           */
+emb_status emb_join(emb_ctx* ctx, emb_stream_t stream);
+
+/* Per-kernel CUDA-event timing: when enabled, every kernel launch is
+ * bracketed by events on its own stream.  emb_profile_read synchronises,
+ * returns the summed milliseconds and launch counts per emb_kernel_kind
+ * (arrays of EMB_NUM_KERNELS), and clears the record.                       */
+emb_status emb_profile(emb_ctx* ctx, int32_t enable);
+emb_status emb_profile_read(emb_ctx* ctx, double* ms, int64_t* count);
 
 /* Synchronise the device and read the counters of the last iteration.       */
 emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out);

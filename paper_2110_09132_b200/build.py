@@ -60,6 +60,8 @@ def build(force=False, verbose=False):
     inc, libdir = _nccl_dirs()
     nvcc = _nvcc()
     common = ARCH + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", inc]
+    extra = os.environ.get("EMB_NVCC_EXTRA", "").split()  # e.g. -DEMB_PHASE_TIMING (profiling builds)
+    common += extra
 
     def comp(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

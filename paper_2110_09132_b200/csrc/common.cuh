@@ -14,6 +14,10 @@ enum Mode { RAW = 0, COAL = 1, SPLIT = 2 };
 enum Optim { SGD = 0, ADAM = 1 };
 enum DType { F32 = 0, BF16 = 1 };
 enum ErrBit { ERR_ID = 1, ERR_STATE = 2, ERR_TIMEOUT = 4 };
+// counts[p][n][CNT_W]: T, u, p, nchunks, nlong are written by route and read
+// by the backward kernels; ST / SU are the sort's own copies (the sort of the
+// next batch may run while the scheduled merge still reads u / p).
+enum CountSlot { CNT_T = 0, CNT_U = 1, CNT_P = 2, CNT_NCH = 3, CNT_NLONG = 4, CNT_ST = 5, CNT_SU = 6, CNT_W = 8 };
 
 // Peer-written flags living in every rank's NVLink-visible region.  Slot [n]
 // is written only by rank n (epoch values = iteration number t, monotone).
@@ -29,9 +33,9 @@ struct Flags {
 
 // Byte offsets inside the symmetric (IPC-exported) region; identical on every rank.
 struct SymLayout {
-  size_t shard;   // [L][d]            table dtype     (peers read: forward pull)
-  size_t gids;    // [2][N][max_tok]   int32           (peers write: id all-gather)
-  size_t ntok;    // [2][N]            int32
+  size_t shard;   // [L][d]             table dtype     (peers read: forward pull)
+  size_t gids;    // [2][N][max_tok]    int32           (peers write: id all-gather)
+  size_t ntok;    // [2][N]             int32
   size_t recv;    // [2][N][max_tok][d] wire = table dtype (senders write: grad AlltoAll)
   size_t flags;   // Flags
   size_t total;
@@ -50,6 +54,7 @@ struct DevCtx {
   unsigned long long timeout_ns;
   int C;                  // rows per reduce chunk
   int max_chunks;         // per source per parity
+  int max_long;           // multi-chunk slots per source per parity (<= max_tok / (C+1) + 1)
   int idbits, posbits;
 
   char* sym[EMB_WMAX];    // base of every rank's symmetric region (own included)
@@ -58,24 +63,36 @@ struct DevCtx {
   // local (not peer-visible)
   float* adam_m;          // [L][d]
   float* adam_v;          // [L][d]
-  int* nextmark;          // [L]       epoch tag: id in D_next of iteration v  <=> nextmark[id] == v+1
-  unsigned long long* slotmap;  // [L][N] (t << 32) | slot  — source n holds id in slot k at iteration t
-  int* perm;              // [2][N][max_tok]    positions sorted by (id, pos)
-  int* slot_id;           // [2][N][max_tok]    slot k -> id   (prior asc, then scheduled asc)
+  unsigned long long* slotmap;  // [L][N] (t << 32) | slot — source n holds id in slot k at iteration t (N > 1)
+  int* perm;              // [2][N][max_tok]    positions sorted by (dropped, id, position)
+  int* uid;               // [2][N][max_tok]    ascending unique kept ids (sort output)
+  int* useg;              // [2][N][max_tok+1]  unique index -> first index into perm
+  int* slot_id;           // [2][N][max_tok]    slot k -> id
   int* seg_start;         // [2][N][max_tok]    slot k -> first index into perm
   int* seg_end;           // [2][N][max_tok]    slot k -> one past last
   int* chunk_off;         // [2][N][max_tok+1]  slot k -> first chunk
   int* chunk_slot;        // [2][N][max_chunks] chunk -> slot
-  int* counts;            // [2][N][4]          T, u, p (prior slots), nchunks
-  int* slot_ctr;          // [2][N][max_tok]    arrivals of multi-chunk slots
-  float* scratch;         // [2][N][max_chunks][dw]  multi-chunk partials (dw = D for sender, d for RAW owner)
-  char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (wire dtype)
+  int* long_slots;        // [2][N][max_long]   slots with more than one chunk
+  int* counts;            // [2][N][CNT_W]      T, u, p, nchunks, nlong
+  float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
+  char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
-  unsigned int* done_ctr; // [32]  last-block counters, one per kernel kind
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
   int* err;               // sticky error bits
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
+  unsigned long long* dbg_ts; // [64] phase timestamps (EMB_PHASE_TIMING builds only)
 };
+
+#ifdef EMB_PHASE_TIMING
+#define EMB_TS(i)                                                       \
+  do {                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x == 0) c.dbg_ts[i] = globaltimer(); \
+  } while (0)
+#else
+#define EMB_TS(i) \
+  do {            \
+  } while (0)
+#endif
 
 // ----------------------------------------------------------------- addressing
 __device__ __forceinline__ char* shard_of(const DevCtx& c, int s) { return c.sym[s] + c.lay.shard; }
@@ -92,6 +109,9 @@ __device__ __forceinline__ Flags* flags_of(const DevCtx& c, int s) {
   return reinterpret_cast<Flags*>(c.sym[s] + c.lay.flags);
 }
 __device__ __forceinline__ size_t pn(const DevCtx& c, int p, int n) { return (size_t)(p * c.N + n); }
+__device__ __forceinline__ const int* counts_of(const DevCtx& c, int p, int n) {
+  return c.counts + pn(c, p, n) * CNT_W;
+}
 
 // ----------------------------------------------------------------- memory model
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -113,7 +133,7 @@ __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag,
   if ((int)(ld_acquire_sys(flag) - target) >= 0) return;
   unsigned long long t0 = globaltimer();
   while ((int)(ld_acquire_sys(flag) - target) < 0) {
-    __nanosleep(64);
+    __nanosleep(32);
     if (globaltimer() - t0 > c.timeout_ns) {
       atomicOr(c.err, ERR_TIMEOUT);
       return;
@@ -121,32 +141,28 @@ __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag,
   }
 }
 
-// Block-level: thread 0 waits for flag[s] >= target for every rank s, then the
-// block proceeds.  (Grids that wait are bounded to be co-resident.)
-__device__ __forceinline__ void block_wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target) {
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < c.N; ++s) wait_flag(c, flags + s, target);
-  }
-  __syncthreads();
+// Thread-level: wait for flags[s] >= target for every rank s.
+// N == 1: every producer/consumer pair is ordered by the stream or an event,
+// so the flag protocol (and its system fences) is skipped entirely.
+__device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target) {
+  if (c.N == 1) return;
+  for (int s = 0; s < c.N; ++s) wait_flag(c, flags + s, target);
 }
 
-// Last-block pattern: every block calls this after its stores; returns true in
-// exactly one thread (thread 0 of the last block to arrive), after a system
-// fence, so it may publish flags that cover every block's stores.
-__device__ __forceinline__ bool last_block_done(unsigned int* ctr) {
-  __syncthreads();
-  bool last = false;
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    unsigned int prev = atomicAdd(ctr, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence_system();
-      *ctr = 0u;  // re-arm for the next launch (stream-ordered)
-      last = true;
-    }
+// Publish value v into slot [c.r] of field `field` (an offset into Flags) of
+// every rank's flags.  Called by ONE thread at the start of the kernel that
+// follows the producer on the same stream: the producer has completed, so its
+// stores (local and peer) are performed; the system fence + release store make
+// them visible to the peer before the flag.
+__device__ __forceinline__ void publish(const DevCtx& c, size_t field_off, uint32_t v) {
+  if (c.N == 1) return;
+  __threadfence_system();
+  for (int s = 0; s < c.N; ++s) {
+    uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(flags_of(c, s)) + field_off) + c.r;
+    st_release_sys(f, v);
   }
-  return last;
 }
+#define EMB_FLAG_OFF(member) offsetof(::emb::Flags, member)
 
 // ----------------------------------------------------------------- vector access
 __device__ __forceinline__ uint4 ld16(const void* p) { return *reinterpret_cast<const uint4*>(p); }
@@ -157,6 +173,7 @@ __device__ __forceinline__ uint4 ld16_nc(const void* p) {
                : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint4 ld16_cg(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ void st16(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
 
 // 16 bytes -> floats (EPV = 4 for fp32, 8 for bf16)
@@ -176,7 +193,7 @@ struct Vec<F32> {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t bf_pack2(float a, float b) {
-  // round-to-nearest-even to bf16 (cvt.rn.bf16x2.f32 packs hi=first operand)
+  // round-to-nearest-even to bf16 (cvt.rn.bf16x2.f32 d, hi, lo)
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
   return r;

@@ -30,9 +30,9 @@ int bits_for(long long v) {  // bits needed to represent value v (v >= 0)
 }
 
 struct Plan {
-  int N, r, d, esz, cpr, cps, C, max_chunks, idbits, posbits;
+  int N, r, d, esz, cpr, cps, C, max_chunks, max_long, idbits, posbits;
   bool key64;
-  size_t route_smem;
+  size_t sort_smem, route_smem;
   SymLayout lay;
   size_t local_bytes;
 };
@@ -59,11 +59,13 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (pl->cpr > 256) return EMB_ERR_SHAPE;  // rows up to 4 KB
   pl->C = 16;
   pl->max_chunks = cfg->max_tokens + cfg->max_tokens / pl->C + 1;
+  pl->max_long = cfg->max_tokens / (pl->C + 1) + 1;
   pl->idbits = bits_for(cfg->vocab);  // the value L itself is the invalid-id sentinel
   pl->posbits = bits_for(cfg->max_tokens - 1);
-  pl->key64 = pl->idbits + pl->posbits > 32;
-  pl->route_smem = route_smem_bytes(cfg->max_tokens, pl->key64);
-  if (pl->route_smem > 227 * 1024) return EMB_ERR_CAPACITY;
+  pl->key64 = 1 + pl->idbits + pl->posbits > 32;  // dropped bit | id | pos
+  pl->sort_smem = sort_smem_bytes(cfg->max_tokens, pl->key64);
+  pl->route_smem = route_smem_bytes(cfg->vocab);
+  if (pl->sort_smem > 227 * 1024 || pl->route_smem > 227 * 1024) return EMB_ERR_CAPACITY;
 
   const size_t L = (size_t)cfg->vocab, T = (size_t)cfg->max_tokens;
   SymLayout& y = pl->lay;
@@ -77,10 +79,10 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
 
   size_t loc = 0;
   if (cfg->optim == EMB_ADAM) loc += 2 * L * pl->d * 4;
-  loc += L * 4 + L * N * 8;
-  loc += 4 * 2 * N * T * 4 + 2 * N * (T + 1) * 4 + 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * 16;
-  loc += 2 * N * T * 4 + 2 * (size_t)pl->max_chunks * cfg->dim * 4;
-  if (cfg->mode == EMB_BWD_SPLIT) loc += 2 * T * cfg->dim * pl->esz;
+  if (N > 1) loc += L * N * 8;
+  loc += 4 * 2 * N * T * 4 + 2 * N * (T + 1) * 4 + 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * CNT_W * 4;
+  loc += 2 * N * (size_t)pl->max_long * 4 + 2 * (size_t)pl->max_chunks * cfg->dim * 4;
+  if (cfg->mode == EMB_BWD_SPLIT && N > 1) loc += 2 * T * cfg->dim * pl->esz;
   if (cfg->mode == EMB_BWD_RAW) loc += 2 * N * T * pl->d * 4;
   pl->local_bytes = loc;
   return EMB_OK;
@@ -98,15 +100,41 @@ struct emb_ctx {
   char* sym = nullptr;
   bool peer_open[EMB_MAX_WORLD] = {};
   std::vector<void*> allocs;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {};
+  cudaStream_t side = nullptr;  // scheduled part (lowest priority)
+  cudaStream_t aux = nullptr;   // per-source sort of the next batch (overlaps the current iteration)
+  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {};
   bool def_pending[2] = {false, false};
+  bool sort_pending[2] = {false, false};
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
+  bool fwd_pushed = false;   // last forward pushed its ids (route publishes them)
   int last_n = 0;
   DenseQueue* dq = nullptr;
+  long long launches = 0;
+  bool prof = false;
+  struct ProfRec { int kind; cudaEvent_t a, b; };
+  std::vector<ProfRec> prof_recs;
 };
+
+// Launch one kernel through `fn`, counting it and (when profiling) bracketing
+// it with CUDA events on its own stream.
+template <typename F>
+static cudaError_t run_k(emb_ctx* ctx, int kind, cudaStream_t s, F&& fn) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (ctx->prof) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  cudaError_t e = fn();
+  ctx->launches += 1;
+  if (ctx->prof) {
+    cudaEventRecord(b, s);
+    ctx->prof_recs.push_back({kind, a, b});
+  }
+  return e;
+}
 
 #define CKC(ctx, call)                                                                   \
   do {                                                                                  \
@@ -186,7 +214,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   c.lr = cfg->lr; c.beta1 = cfg->beta1; c.beta2 = cfg->beta2; c.eps = cfg->eps;
   c.scale = cfg->grad_scale != 0.f ? cfg->grad_scale : 1.0f / (float)pl.N;
   c.timeout_ns = (unsigned long long)(cfg->timeout_ms > 0 ? cfg->timeout_ms : 10000) * 1000000ull;
-  c.C = pl.C; c.max_chunks = pl.max_chunks; c.idbits = pl.idbits; c.posbits = pl.posbits;
+  c.C = pl.C; c.max_chunks = pl.max_chunks; c.max_long = pl.max_long; c.idbits = pl.idbits; c.posbits = pl.posbits;
   c.lay = pl.lay;
 
 #define ALLOC(ptr, bytes) \
@@ -203,34 +231,38 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
       ALLOC(c.adam_m, L * pl.d * 4);
       ALLOC(c.adam_v, L * pl.d * 4);
     }
-    ALLOC(c.nextmark, L * 4);
-    ALLOC(c.slotmap, L * N * 8);
+    if (N > 1) ALLOC(c.slotmap, L * N * 8);
     ALLOC(c.perm, 2 * N * T * 4);
+    ALLOC(c.uid, 2 * N * T * 4);
+    ALLOC(c.useg, 2 * N * (T + 1) * 4);
     ALLOC(c.slot_id, 2 * N * T * 4);
     ALLOC(c.seg_start, 2 * N * T * 4);
     ALLOC(c.seg_end, 2 * N * T * 4);
     ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
     ALLOC(c.chunk_slot, 2 * N * (size_t)pl.max_chunks * 4);
-    ALLOC(c.counts, 2 * N * 4 * 4);
-    ALLOC(c.slot_ctr, 2 * N * T * 4);
+    ALLOC(c.long_slots, 2 * N * (size_t)pl.max_long * 4);
+    ALLOC(c.counts, 2 * N * CNT_W * 4);
     ALLOC(c.scratch, 2 * (size_t)pl.max_chunks * cfg->dim * 4);
-    if (cfg->mode == EMB_BWD_SPLIT) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
+    if (cfg->mode == EMB_BWD_SPLIT && N > 1) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
     if (cfg->mode == EMB_BWD_RAW) ALLOC(c.gc_owner, 2 * N * T * pl.d * 4);
-    ALLOC(c.done_ctr, 32 * 4);
     ALLOC(c.t_rec, 2 * 4);
     ALLOC(c.err, 4);
     ALLOC(c.stats, 3 * N * 8);
+    ALLOC(c.dbg_ts, 64 * 8);
   }
 #undef ALLOC
-  if (route_set_smem(pl.key64, pl.route_smem) != cudaSuccess) goto fail;
+  if (route_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem, pl.route_smem) != cudaSuccess) goto fail;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
     if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo) != cudaSuccess) goto fail;
+    if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
   }
   for (int i = 0; i < 2; ++i) {
     if (cudaEventCreateWithFlags(&ctx->ev_prior[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_def[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+    if (cudaEventCreateWithFlags(&ctx->ev_main[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+    if (cudaEventCreateWithFlags(&ctx->ev_sorted[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
   *out = ctx;
@@ -321,7 +353,19 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->it += 1;
   const int p = (int)(ctx->it & 1);
   if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
-  CKC(ctx, launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, ctx->prefetched ? 1 : 0, stream));
+  const int pre = ctx->prefetched ? 1 : 0;
+  CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
+  if (!pre) {
+    // ids were not prefetched: sort them now on the auxiliary stream (the
+    // forward pushed them; the sort publishes the push to the peers)
+    CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
+    CKC(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_main[p], 0));
+    CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux, [&] {
+      return launch_sort(ctx->dc, p, 1, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
+    }));
+    CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], ctx->aux));
+    ctx->sort_pending[p] = true;
+  }
   ctx->prefetched = false;
   ctx->last_n = n;
   ctx->state = ST_AFTER_FWD;
@@ -340,21 +384,39 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   const int p = (int)(ctx->it & 1);
   const DevCtx& c = ctx->dc;
   const int mode = ctx->cfg.mode;
-  CKC(ctx, launch_ids(c, ctx->lc, next_ids, n_next, p, (mode == EMB_BWD_SPLIT && next_ids) ? 1 : 0, stream));
-  CKC(ctx, launch_route(c, ctx->lc, p, ctx->pl.key64, ctx->pl.route_smem, stream));
+  const LaunchCfg& lc = ctx->lc;
+  const int last_n = ctx->last_n;
+  cudaStream_t side = ctx->side;
+  cudaStream_t aux = ctx->aux;
+  if (ctx->sort_pending[p]) {  // the sort of this batch (aux stream) must be complete
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
+    ctx->sort_pending[p] = false;
+  }
+  CKC(ctx, run_k(ctx, EMB_K_ROUTE, stream,
+                 [&] { return launch_route(c, p, next_ids, n_next, ctx->pl.route_smem, stream); }));
+  if (next_ids) {
+    // prefetch: route pushed the next batch's ids; sort them now, overlapping
+    // the rest of this iteration and the next forward
+    CKC(ctx, cudaEventRecord(ctx->ev_main[p ^ 1], stream));
+    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p ^ 1], 0));
+    CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] { return launch_sort(c, p ^ 1, 0, ctx->pl.key64, ctx->pl.sort_smem, aux); }));
+    CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
+    ctx->sort_pending[p ^ 1] = true;
+  }
   if (mode == EMB_BWD_RAW) {
-    CKC(ctx, launch_rawpush(c, ctx->lc, grad_out, ctx->last_n, p, stream));
-    CKC(ctx, launch_rawcoal(c, ctx->lc, p, stream));
-    CKC(ctx, launch_merge(c, ctx->lc, p, 0, stream));
+    CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
+    CKC(ctx, run_k(ctx, EMB_K_RAWCOAL, stream, [&] { return launch_rawcoal(c, lc, p, stream); }));
+    CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
-    CKC(ctx, launch_coal(c, ctx->lc, grad_out, p, stream));
-    CKC(ctx, launch_merge(c, ctx->lc, p, 0, stream));
+    CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
+    CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
     if (mode == EMB_BWD_SPLIT) {
       // scheduled part: lowest-priority side stream, after the prior part
       CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));
-      CKC(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_prior[p], 0));
-      CKC(ctx, launch_defpush(c, ctx->lc, p, ctx->side));
-      CKC(ctx, launch_merge(c, ctx->lc, p, 1, ctx->side));
+      CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));
+      if (ctx->pl.N > 1)  // N == 1: coal wrote every row to its receive slot directly
+        CKC(ctx, run_k(ctx, EMB_K_DEFPUSH, side, [&] { return launch_defpush(c, lc, p, side); }));
+      CKC(ctx, run_k(ctx, EMB_K_MERGE1, side, [&] { return launch_merge(c, lc, p, 1, side); }));
       CKC(ctx, cudaEventRecord(ctx->ev_def[p], ctx->side));
       ctx->def_pending[p] = true;
     }
@@ -406,8 +468,8 @@ emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream_) {
   if (st != EMB_OK) return st;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
-  for (int p = 0; p < 2; ++p)
-    if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+  st = emb_join(ctx, stream_);
+  if (st != EMB_OK) return st;
   if (ctx->dq) {
     st = dense_queue_flush_all(ctx->dq);
     if (st != EMB_OK) { ctx->poisoned = st; return st; }
@@ -416,6 +478,50 @@ emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream_) {
   }
   CKC(ctx, cudaStreamSynchronize(stream));
   return sticky_err(ctx);
+}
+
+emb_status emb_join(emb_ctx* ctx, emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  for (int p = 0; p < 2; ++p) {
+    if (ctx->def_pending[p]) {
+      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+      ctx->def_pending[p] = false;  // later work on `stream` is ordered after it
+    }
+    if (ctx->sort_pending[p]) {
+      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
+      ctx->sort_pending[p] = false;
+    }
+  }
+  return EMB_OK;
+}
+
+emb_status emb_profile(emb_ctx* ctx, int32_t enable) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  ctx->prof = enable != 0;
+  return EMB_OK;
+}
+
+emb_status emb_profile_read(emb_ctx* ctx, double* ms, int64_t* count) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!ms || !count) return EMB_ERR_INVALID_ARG;
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  CKC(ctx, cudaDeviceSynchronize());
+  for (int k = 0; k < EMB_NUM_KERNELS; ++k) { ms[k] = 0.0; count[k] = 0; }
+  for (auto& r : ctx->prof_recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      ms[r.kind] += t;
+      count[r.kind] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->prof_recs.clear();
+  return EMB_OK;
 }
 
 emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out) {
@@ -430,13 +536,13 @@ emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out) {
   out->world = N;
   if (ctx->bwd_done > 0) {
     const int p = (int)(ctx->it & 1);
-    std::vector<int> cnt(N * 4);
-    CKC(ctx, cudaMemcpy(cnt.data(), ctx->dc.counts + (size_t)p * N * 4, N * 16, cudaMemcpyDeviceToHost));
+    std::vector<int> cnt(N * CNT_W);
+    CKC(ctx, cudaMemcpy(cnt.data(), ctx->dc.counts + (size_t)p * N * CNT_W, N * CNT_W * 4, cudaMemcpyDeviceToHost));
     for (int n = 0; n < N; ++n) {
-      out->n_tokens[n] = cnt[n * 4 + 0];
-      out->u[n] = cnt[n * 4 + 1];
-      out->p[n] = cnt[n * 4 + 2];
-      out->q[n] = cnt[n * 4 + 1] - cnt[n * 4 + 2];
+      out->n_tokens[n] = cnt[n * CNT_W + CNT_T];
+      out->u[n] = cnt[n * CNT_W + CNT_U];
+      out->p[n] = cnt[n * CNT_W + CNT_P];
+      out->q[n] = cnt[n * CNT_W + CNT_U] - cnt[n * CNT_W + CNT_P];
     }
   }
   std::vector<unsigned long long> s(3 * N);
@@ -447,6 +553,7 @@ emb_status emb_get_stats(emb_ctx* ctx, emb_stats* out) {
     out->ids_bytes_pushed[n] = (int64_t)s[2 * N + n];
   }
   CKC(ctx, cudaMemcpy(&out->err_flags, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
+  out->kernel_launches = ctx->launches;
   return EMB_OK;
 }
 
@@ -458,6 +565,12 @@ emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, s
   *n = 0;
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
   CKC(ctx, cudaDeviceSynchronize());
+  if (item == EMB_DBG_TIMESTAMPS) {
+    *n = 64;
+    if (cap < 64 * 8) return EMB_ERR_CAPACITY;
+    CKC(ctx, cudaMemcpy(host, ctx->dc.dbg_ts, 64 * 8, cudaMemcpyDeviceToHost));
+    return EMB_OK;
+  }
   if (item == EMB_DBG_ISSUE_LOG) {
     std::vector<int64_t> log;
     if (ctx->dq) dense_queue_issue_log(ctx->dq, &log);
@@ -471,12 +584,16 @@ emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, s
   if (item == EMB_DBG_COUNTS) {
     *n = (size_t)N * 4;
     if (cap < *n * 4) return EMB_ERR_CAPACITY;
-    CKC(ctx, cudaMemcpy(host, ctx->dc.counts + (size_t)p * N * 4, N * 16, cudaMemcpyDeviceToHost));
+    std::vector<int> all(N * CNT_W);
+    CKC(ctx, cudaMemcpy(all.data(), ctx->dc.counts + (size_t)p * N * CNT_W, N * CNT_W * 4, cudaMemcpyDeviceToHost));
+    int* h = static_cast<int*>(host);
+    for (int q = 0; q < N; ++q)
+      for (int j = 0; j < 4; ++j) h[q * 4 + j] = all[q * CNT_W + j];
     return EMB_OK;
   }
   if (src < 0 || src >= N) return EMB_ERR_INVALID_ARG;
-  int cnt[4];
-  CKC(ctx, cudaMemcpy(cnt, ctx->dc.counts + ((size_t)p * N + src) * 4, 16, cudaMemcpyDeviceToHost));
+  int cnt[CNT_W];
+  CKC(ctx, cudaMemcpy(cnt, ctx->dc.counts + ((size_t)p * N + src) * CNT_W, CNT_W * 4, cudaMemcpyDeviceToHost));
   const int* dptr = nullptr;
   size_t len = 0;
   const size_t off = ((size_t)p * N + src) * ctx->cfg.max_tokens;
@@ -525,9 +642,12 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   for (int i = 0; i < 2; ++i) {
     if (ctx->ev_prior[i]) cudaEventDestroy(ctx->ev_prior[i]);
     if (ctx->ev_def[i]) cudaEventDestroy(ctx->ev_def[i]);
+    if (ctx->ev_main[i]) cudaEventDestroy(ctx->ev_main[i]);
+    if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
   }
   delete ctx;
   return EMB_OK;

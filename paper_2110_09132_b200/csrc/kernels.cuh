@@ -4,26 +4,33 @@
 
 namespace emb {
 
-// done_ctr slots (one per kernel kind that uses the last-block pattern)
-enum DoneSlot { K_FWD_IDS = 0, K_IDS = 1, K_COAL = 2, K_DEFPUSH = 3, K_RAWPUSH = 4, K_MERGE0 = 5, K_MERGE1 = 6 };
-
 struct LaunchCfg {
   int nsm;  // SM count of the device
 };
 
-// a1-a4: forward (ids all-gather push or prefetch check, wait, pull-gather)
+// Flag publication protocol: a kernel never
+// fences its own stores; the NEXT kernel on the same stream (or one ordered
+// after it by an event), which starts only after the producer completed,
+// publishes the producer's flag to every peer (one thread, one system fence),
+// then waits for the peers' flags.  N == 1 skips the protocol (stream order).
+
+// a1-a4: forward (publish prior_done/def_done of earlier iterations, id push or
+// prefetch check, wait for every owner, pull-gather)
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
                        int prefetched, cudaStream_t s);
-// a5: push next ids to every peer, wait, mark D_next (epoch tags)
-cudaError_t launch_ids(const DevCtx& c, const LaunchCfg& L, const int* next_ids, int n_next, int p,
-                       int do_mark, cudaStream_t s);
-// a6 + a8: per-source sort / unique / Alg. 1 split / routing (one CTA per source)
-cudaError_t launch_route(const DevCtx& c, const LaunchCfg& L, int p, bool key64, size_t smem, cudaStream_t s);
-size_t route_smem_bytes(int max_tok, bool key64);
-cudaError_t route_set_smem(bool key64, size_t smem);
-// a7 + a9 (+a10 for the prior part): sender coalesce; prior rows pushed to owners, scheduled rows staged
+// a6: per-source sort by (dropped, id, position) + unique ids (auxiliary stream)
+cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size_t smem, cudaStream_t s);
+// a5 + a8: prefetch all-gather of the next ids, D_next bitmap, Alg. 1 split of
+// every source's unique ids into prior / scheduled slots, reduce chunks
+cudaError_t launch_route(const DevCtx& c, int p, const int* next_ids, int n_next, size_t smem, cudaStream_t s);
+size_t sort_smem_bytes(int max_tok, bool key64);
+size_t route_smem_bytes(long long vocab);
+cudaError_t route_set_smem(int max_tok, bool key64, size_t sort_smem, size_t route_smem);
+// a7 + a9 (+a10 for the prior part): sender coalesce.  coal_a: one warp per
+// chunk of <= C rows (single-chunk slots emitted directly, others leave fp32
+// partials); coal_b: one CTA per multi-chunk slot, fixed-order combine.
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s);
-// a12: push the staged scheduled rows to their owners
+// a12: push the staged scheduled rows to their owners (N > 1)
 cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
 // RAW a7/a10: push raw dY column slices; owner-side per-source coalesce
 cudaError_t launch_rawpush(const DevCtx& c, const LaunchCfg& L, const void* dY, int n, int p, cudaStream_t s);

@@ -24,15 +24,15 @@ STATUS = {0: "EMB_OK", 1: "EMB_ERR_INVALID_ARG", 2: "EMB_ERR_SHAPE", 3: "EMB_ERR
 EMB_FP32, EMB_BF16 = 0, 1
 EMB_SGD, EMB_ADAM = 0, 1
 EMB_BWD_RAW, EMB_BWD_COAL, EMB_BWD_SPLIT = 0, 1, 2
-EMB_DBG_GIDS, EMB_DBG_SLOT_IDS, EMB_DBG_COUNTS, EMB_DBG_PERM, EMB_DBG_ISSUE_LOG = range(5)
+EMB_DBG_GIDS, EMB_DBG_SLOT_IDS, EMB_DBG_COUNTS, EMB_DBG_PERM, EMB_DBG_ISSUE_LOG, EMB_DBG_TIMESTAMPS = range(6)
 EMB_STATE_SHARD, EMB_STATE_ADAM_M, EMB_STATE_ADAM_V = range(3)
 MODES = {"raw": EMB_BWD_RAW, "coal": EMB_BWD_COAL, "split": EMB_BWD_SPLIT}
 
 EXPORTED = [
     "emb_status_str", "emb_workspace_bytes", "emb_create", "emb_ipc_handle", "emb_get_unique_id",
     "emb_shard_init", "emb_forward_exchange", "emb_backward_exchange", "dense_allreduce_enqueue",
-    "dense_queue_flush", "dense_wait", "emb_flush", "emb_get_stats", "emb_debug_copy", "emb_state_ptr",
-    "emb_queue_issue_order", "emb_shard_destroy",
+    "dense_queue_flush", "dense_wait", "emb_flush", "emb_join", "emb_profile", "emb_profile_read",
+    "emb_get_stats", "emb_debug_copy", "emb_state_ptr", "emb_queue_issue_order", "emb_shard_destroy",
 ]
 
 
@@ -58,7 +58,12 @@ class EmbStats(ctypes.Structure):
                 ("n_tokens", ctypes.c_int32 * W), ("u", ctypes.c_int32 * W), ("p", ctypes.c_int32 * W),
                 ("q", ctypes.c_int32 * W), ("fwd_bytes_pulled", ctypes.c_int64 * W),
                 ("bwd_bytes_pushed", ctypes.c_int64 * W), ("ids_bytes_pushed", ctypes.c_int64 * W),
-                ("err_flags", ctypes.c_int32)]
+                ("err_flags", ctypes.c_int32), ("kernel_launches", ctypes.c_int64)]
+
+
+KERNEL_NAMES = ["fwd_pull_gather", "sort_unique", "route_split", "coal_push", "merge_update_prior",
+                "defpush", "merge_update_sched", "rawpush", "rawcoal"]
+EMB_NUM_KERNELS = len(KERNEL_NAMES)
 
 
 _lib_handle = None
@@ -87,6 +92,9 @@ def lib():
             "dense_queue_flush": [vp],
             "dense_wait": [vp, i64, vp],
             "emb_flush": [vp, vp],
+            "emb_join": [vp, vp],
+            "emb_profile": [vp, i32],
+            "emb_profile_read": [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)],
             "emb_get_stats": [vp, ctypes.POINTER(EmbStats)],
             "emb_debug_copy": [vp, i32, i32, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
             "emb_state_ptr": [vp, i32, ctypes.POINTER(vp)],
@@ -199,6 +207,22 @@ def emb_flush(ctx, stream=None):
     _ck(lib().emb_flush(ctx, _stream(stream)), "emb_flush")
 
 
+def emb_join(ctx, stream=None):
+    _ck(lib().emb_join(ctx, _stream(stream)), "emb_join")
+
+
+def emb_profile(ctx, enable):
+    _ck(lib().emb_profile(ctx, 1 if enable else 0), "emb_profile")
+
+
+def emb_profile_read(ctx):
+    """{kernel name: (total ms, launches)} since profiling was enabled."""
+    ms = (ctypes.c_double * EMB_NUM_KERNELS)()
+    cnt = (ctypes.c_int64 * EMB_NUM_KERNELS)()
+    _ck(lib().emb_profile_read(ctx, ms, cnt), "emb_profile_read")
+    return {KERNEL_NAMES[k]: (ms[k], cnt[k]) for k in range(EMB_NUM_KERNELS) if cnt[k]}
+
+
 def emb_get_stats(ctx):
     s = EmbStats()
     _ck(lib().emb_get_stats(ctx, ctypes.byref(s)), "emb_get_stats")
@@ -206,11 +230,11 @@ def emb_get_stats(ctx):
     return {"iter": s.iter, "world": N, "n_tokens": list(s.n_tokens[:N]), "u": list(s.u[:N]),
             "p": list(s.p[:N]), "q": list(s.q[:N]), "fwd_bytes_pulled": list(s.fwd_bytes_pulled[:N]),
             "bwd_bytes_pushed": list(s.bwd_bytes_pushed[:N]), "ids_bytes_pushed": list(s.ids_bytes_pushed[:N]),
-            "err_flags": s.err_flags}
+            "err_flags": s.err_flags, "kernel_launches": s.kernel_launches}
 
 
 def emb_debug_copy(ctx, item, src=0, cap_elems=1 << 22):
-    dt = np.int64 if item == EMB_DBG_ISSUE_LOG else np.int32
+    dt = np.int64 if item in (EMB_DBG_ISSUE_LOG, EMB_DBG_TIMESTAMPS) else np.int32
     buf = np.zeros(cap_elems, dtype=dt)
     n = ctypes.c_size_t()
     _ck(lib().emb_debug_copy(ctx, item, src, buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes, ctypes.byref(n)),

@@ -86,8 +86,15 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
             for n in range(N):
                 ids_n = np.asarray(wl.ids[k][n], np.int64)
                 assert np.array_equal(ex.debug(E.EMB_DBG_GIDS, n), ids_n), f"iter {t}: gathered ids of {n}"
-                assert np.array_equal(ex.debug(E.EMB_DBG_PERM, n), np.argsort(ids_n, kind="stable")), \
-                    f"iter {t}: perm of {n}"
+                # perm: positions sorted by (dropped, id, position); dropped = pad when pad_id >= 0
+                drop = (ids_n == pad_id) if pad_id >= 0 else np.zeros(ids_n.size, bool)
+                want_perm = np.lexsort((np.arange(ids_n.size), ids_n, drop))
+                got_perm = ex.debug(E.EMB_DBG_PERM, n)
+                if not np.array_equal(got_perm, want_perm):
+                    bad = np.flatnonzero(got_perm != want_perm)[:6] if got_perm.size == want_perm.size else []
+                    raise AssertionError(f"iter {t}: perm of {n}: sizes {got_perm.size}/{want_perm.size}, "
+                                         f"first diffs at {list(bad)}: got {got_perm[bad]} want {want_perm[bad]}; "
+                                         f"ids there {ids_n[want_perm[bad]]} / {ids_n[got_perm[bad]]}")
                 want = np.concatenate([res.P_n[n], res.D_n[n]]).astype(np.int64)
                 got = ex.debug(E.EMB_DBG_SLOT_IDS, n)
                 assert np.array_equal(got, want), f"iter {t}: slot ids of source {n}: {got[:8]} vs {want[:8]}"
