@@ -78,6 +78,7 @@ struct DevCtx {
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
+  float* alpha;           // [2]   Adam step size alpha_t of the iteration using parity p (route computes it once)
   int* err;               // sticky error bits
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
   unsigned long long* dbg_ts; // [64] phase timestamps (EMB_PHASE_TIMING builds only)
@@ -163,6 +164,16 @@ __device__ __forceinline__ void publish(const DevCtx& c, size_t field_off, uint3
   }
 }
 #define EMB_FLAG_OFF(member) offsetof(::emb::Flags, member)
+
+// ----------------------------------------------------------------- programmatic dependent launch
+// Every exchange kernel is launched with the PDL attribute: its grid may start
+// while the previous kernel on the stream drains; griddepcontrol.wait (first
+// thing in every kernel) blocks until that kernel has completed and its
+// memory is visible, and launch_dependents (at the end of every CTA) lets the
+// next kernel's launch overlap this one's tail.  Without the attribute both
+// are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ----------------------------------------------------------------- vector access
 __device__ __forceinline__ uint4 ld16(const void* p) { return *reinterpret_cast<const uint4*>(p); }

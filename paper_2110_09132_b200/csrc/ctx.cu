@@ -246,6 +246,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cfg->mode == EMB_BWD_SPLIT && N > 1) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
     if (cfg->mode == EMB_BWD_RAW) ALLOC(c.gc_owner, 2 * N * T * pl.d * 4);
     ALLOC(c.t_rec, 2 * 4);
+    ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
     ALLOC(c.stats, 3 * N * 8);
     ALLOC(c.dbg_ts, 64 * 8);

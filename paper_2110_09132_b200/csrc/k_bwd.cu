@@ -153,6 +153,7 @@ __device__ __forceinline__ void emit_coal_row(const DevCtx& c, int p, int k, int
 // ------------------------------------------------------------------ sender coalesce
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) coal_a_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+  pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -182,10 +183,12 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_a_kernel(DevCtx c, const cha
       emit_coal_row<DT, V>(c, p, k, Pr, acc);
     }
   }
+  pdl_trigger();
 }
 
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) coal_b_kernel(DevCtx c, int p) {
+  pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][D]
   const int r = c.r;
@@ -217,10 +220,12 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_b_kernel(DevCtx c, int p) {
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ scheduled push (N > 1)
 __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
+  pdl_wait();
   const int r = c.r;
   const int* cnt = counts_of(c, p, r);
   const int U = cnt[CNT_U], Pr = cnt[CNT_P], Q = U - Pr;
@@ -235,10 +240,12 @@ __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
     const int s = c16 / c.cps, cs = c16 - s * c.cps;
     st16(recv_of(c, s, p, r) + (size_t)(Pr + k) * slice_bytes + (size_t)cs * 16, val);
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ RAW mode
 __global__ void __launch_bounds__(BWD_THREADS) rawpush_kernel(DevCtx c, const char* __restrict__ dY, int n, int p) {
+  pdl_wait();
   const int r = c.r;
   const size_t row_bytes = (size_t)c.D * c.esz, slice_bytes = (size_t)c.d * c.esz;
   const size_t total = (size_t)n * c.cpr;
@@ -251,11 +258,13 @@ __global__ void __launch_bounds__(BWD_THREADS) rawpush_kernel(DevCtx c, const ch
     const int s = c16 / c.cps, cs = c16 - s * c.cps;
     st16(recv_of(c, s, p, r) + (size_t)j * slice_bytes + (size_t)cs * 16, val);
   }
+  pdl_trigger();
 }
 
 // owner-side coalesce of every source's raw slices -> gc_owner (fp32)
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p) {
+  pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -288,10 +297,12 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
                            : c.gc_owner + (bpn + k) * (size_t)c.d;
     store_partial<EPV, V>(dst, c.cps, acc);
   }
+  pdl_trigger();
 }
 
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p) {
+  pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][d]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -332,11 +343,13 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p)
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ owner merge + update
 template <int DT, bool RAWSRC>
 __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int part, int G) {
+  pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   const uint32_t t = c.t_rec[p];
   if (!RAWSRC) {
@@ -359,11 +372,7 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       total += cnt[n];
     }
   }
-  float alpha = 0.f;
-  if (c.optim == ADAM) {
-    const double td = (double)t;
-    alpha = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
-  }
+  const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;  // computed once by route(t)
   const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int grp = gtid / G, gl = gtid - grp * G, ngrp = (gridDim.x * blockDim.x) / G;
@@ -453,6 +462,7 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       st16(wp, Vec<DT>::pack(w));
     }
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ launchers
@@ -463,33 +473,33 @@ static int grid_for_warps(long long warps, int cap) {
   return (int)blocks;
 }
 
-#define EMB_DISPATCH_V(V_, KERNEL, DT, ...)          \
-  do {                                              \
-    if ((V_) <= 1) KERNEL<DT, 1> __VA_ARGS__;        \
-    else if ((V_) <= 2) KERNEL<DT, 2> __VA_ARGS__;   \
-    else if ((V_) <= 4) KERNEL<DT, 4> __VA_ARGS__;   \
-    else if ((V_) <= 8) KERNEL<DT, 8> __VA_ARGS__;   \
-    else return cudaErrorInvalidValue;              \
-  } while (0)
+// pick the V (16-byte chunks per lane) instantiation and launch it with PDL
+#define EMB_LAUNCH_V(V_, KERNEL, DT, GRID, SMEM, ...)                                                   \
+  ((V_) <= 1   ? launch_pdl(KERNEL<DT, 1>, dim3(GRID), dim3(BWD_THREADS), (SMEM), s, __VA_ARGS__)     \
+   : (V_) <= 2 ? launch_pdl(KERNEL<DT, 2>, dim3(GRID), dim3(BWD_THREADS), (SMEM), s, __VA_ARGS__)     \
+   : (V_) <= 4 ? launch_pdl(KERNEL<DT, 4>, dim3(GRID), dim3(BWD_THREADS), (SMEM), s, __VA_ARGS__)     \
+   : (V_) <= 8 ? launch_pdl(KERNEL<DT, 8>, dim3(GRID), dim3(BWD_THREADS), (SMEM), s, __VA_ARGS__)     \
+               : cudaErrorInvalidValue)
+
+template <int DT>
+static void coal_b_smem(int V, size_t smem) {
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (V <= 1) cudaFuncSetAttribute(coal_b_kernel<DT, 1>, a, (int)smem);
+  else if (V <= 2) cudaFuncSetAttribute(coal_b_kernel<DT, 2>, a, (int)smem);
+  else if (V <= 4) cudaFuncSetAttribute(coal_b_kernel<DT, 4>, a, (int)smem);
+  else cudaFuncSetAttribute(coal_b_kernel<DT, 8>, a, (int)smem);
+}
 
 template <int DT>
 static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
   const int V = (c.cpr + 31) / 32;
   const int ga = grid_for_warps(c.max_chunks, L.nsm * 8);
-  EMB_DISPATCH_V(V, coal_a_kernel, DT, <<<ga, BWD_THREADS, 0, s>>>(c, y, p));
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = EMB_LAUNCH_V(V, coal_a_kernel, DT, ga, 0, c, y, p);
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)BWD_WARPS * c.D * 4;
   const int gb = c.max_long < 1 ? 1 : c.max_long;
-  if (smem > 48 * 1024) {
-    const int a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (V <= 1) cudaFuncSetAttribute(coal_b_kernel<DT, 1>, (cudaFuncAttribute)a, (int)smem);
-    else if (V <= 2) cudaFuncSetAttribute(coal_b_kernel<DT, 2>, (cudaFuncAttribute)a, (int)smem);
-    else if (V <= 4) cudaFuncSetAttribute(coal_b_kernel<DT, 4>, (cudaFuncAttribute)a, (int)smem);
-    else cudaFuncSetAttribute(coal_b_kernel<DT, 8>, (cudaFuncAttribute)a, (int)smem);
-  }
-  EMB_DISPATCH_V(V, coal_b_kernel, DT, <<<gb, BWD_THREADS, smem, s>>>(c, p));
-  return cudaGetLastError();
+  if (smem > 48 * 1024) coal_b_smem<DT>(V, smem);
+  return EMB_LAUNCH_V(V, coal_b_kernel, DT, gb, smem, c, p);
 }
 
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s) {
@@ -502,8 +512,7 @@ cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStrea
   int grid = (int)((work + BWD_THREADS * 4 - 1) / (BWD_THREADS * 4));
   if (grid < 1) grid = 1;
   if (grid > L.nsm * 2) grid = L.nsm * 2;
-  defpush_kernel<<<grid, BWD_THREADS, 0, s>>>(c, p);
-  return cudaGetLastError();
+  return launch_pdl(defpush_kernel, dim3(grid), dim3(BWD_THREADS), 0, s, c, p);
 }
 
 cudaError_t launch_rawpush(const DevCtx& c, const LaunchCfg& L, const void* dY, int n, int p, cudaStream_t s) {
@@ -511,22 +520,19 @@ cudaError_t launch_rawpush(const DevCtx& c, const LaunchCfg& L, const void* dY, 
   int grid = (int)((work + BWD_THREADS * 4 - 1) / (BWD_THREADS * 4));
   if (grid < 1) grid = 1;
   if (grid > L.nsm * 2) grid = L.nsm * 2;
-  rawpush_kernel<<<grid, BWD_THREADS, 0, s>>>(c, static_cast<const char*>(dY), n, p);
-  return cudaGetLastError();
+  return launch_pdl(rawpush_kernel, dim3(grid), dim3(BWD_THREADS), 0, s, c, static_cast<const char*>(dY), n, p);
 }
 
 template <int DT>
 static cudaError_t rawcoal_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
   const int V = (c.cps + 31) / 32;
   const int ga = grid_for_warps((long long)c.N * c.max_chunks, L.nsm * 4);
-  EMB_DISPATCH_V(V, rawcoal_a_kernel, DT, <<<ga, BWD_THREADS, 0, s>>>(c, p));
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = EMB_LAUNCH_V(V, rawcoal_a_kernel, DT, ga, 0, c, p);
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)BWD_WARPS * c.d * 4;
   int gb = c.N * c.max_long;
   if (gb < 1) gb = 1;
-  EMB_DISPATCH_V(V, rawcoal_b_kernel, DT, <<<gb, BWD_THREADS, smem, s>>>(c, p));
-  return cudaGetLastError();
+  return EMB_LAUNCH_V(V, rawcoal_b_kernel, DT, gb, smem, c, p);
 }
 
 cudaError_t launch_rawcoal(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
@@ -542,14 +548,12 @@ cudaError_t launch_merge(const DevCtx& c, const LaunchCfg& L, int p, int part, c
   if (grid < 1) grid = 1;
   if (grid > L.nsm * 4) grid = L.nsm * 4;  // waits inside: bounded
   const bool raw = (c.mode == RAW);
-  if (c.dtype == BF16) {
-    if (raw) merge_kernel<BF16, true><<<grid, BWD_THREADS, 0, s>>>(c, p, part, G);
-    else merge_kernel<BF16, false><<<grid, BWD_THREADS, 0, s>>>(c, p, part, G);
-  } else {
-    if (raw) merge_kernel<F32, true><<<grid, BWD_THREADS, 0, s>>>(c, p, part, G);
-    else merge_kernel<F32, false><<<grid, BWD_THREADS, 0, s>>>(c, p, part, G);
-  }
-  return cudaGetLastError();
+  const dim3 g(grid), b(BWD_THREADS);
+  if (c.dtype == BF16)
+    return raw ? launch_pdl(merge_kernel<BF16, true>, g, b, 0, s, c, p, part, G)
+               : launch_pdl(merge_kernel<BF16, false>, g, b, 0, s, c, p, part, G);
+  return raw ? launch_pdl(merge_kernel<F32, true>, g, b, 0, s, c, p, part, G)
+             : launch_pdl(merge_kernel<F32, false>, g, b, 0, s, c, p, part, G);
 }
 
 }  // namespace emb

@@ -26,6 +26,7 @@ static constexpr int FWD_ROWS = 4;  // rows in flight per warp
 template <int V>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* __restrict__ ids, int n,
                                                           char* __restrict__ out, int p, int prefetched) {
+  pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       }
     }
   }
+  pdl_trigger();
 }
 
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
@@ -111,12 +113,12 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   if (grid > L.nsm * 4) grid = L.nsm * 4;  // waits inside: bounded, leaves room for other streams
   const int V = (c.cpr + 31) / 32;
   char* o = static_cast<char*>(out);
-  if (V <= 1) fwd_kernel<1><<<grid, FWD_THREADS, 0, s>>>(c, ids, n, o, p, prefetched);
-  else if (V <= 2) fwd_kernel<2><<<grid, FWD_THREADS, 0, s>>>(c, ids, n, o, p, prefetched);
-  else if (V <= 4) fwd_kernel<4><<<grid, FWD_THREADS, 0, s>>>(c, ids, n, o, p, prefetched);
-  else if (V <= 8) fwd_kernel<8><<<grid, FWD_THREADS, 0, s>>>(c, ids, n, o, p, prefetched);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  const dim3 g(grid), b(FWD_THREADS);
+  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched);
+  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched);
+  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched);
+  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace emb

@@ -95,6 +95,7 @@ __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {
 // ============================================================== sort (aux stream)
 template <typename K, int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, int fwd_pushed) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int kb = (c.max_tok + 1 + 3) & ~3;  // keys per buffer, 16-byte aligned
   K* keyA = reinterpret_cast<K*>(smem_raw);
@@ -255,12 +256,14 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   __syncthreads();
   if (tid == 0 && (T == 0 || (keyA[T - 1] >> dshift) == 0)) useg[U] = T;
   EMB_TS(23);
+  pdl_trigger();
 }
 
 // ============================================================== route (main stream)
 template <int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) route_kernel(DevCtx c, int p, const int* __restrict__ next_ids,
                                                               int n_next) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw);  // D_next, ceil(L/32) words
   __shared__ int s_tmp[64];
@@ -275,6 +278,11 @@ __global__ void __launch_bounds__(RT_THREADS, 1) route_kernel(DevCtx c, int p, c
   const bool has_next = (next_ids != nullptr);
   const long long L = c.L;
   EMB_TS(0);
+  if (n == 0 && tid == 0 && c.optim == ADAM) {
+    // Adam step size of this iteration, once (PyTorch SparseAdam form, reading R3/R4)
+    const double td = (double)t;
+    c.alpha[p] = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
+  }
 
   // ---- 1. prefetch all-gather: CTA n pushes this rank's next ids to peer n
   if (has_next) {
@@ -448,6 +456,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) route_kernel(DevCtx c, int p, c
   }
   (void)kslot;
   EMB_TS(4);
+  pdl_trigger();
 }
 
 // ============================================================== launchers
@@ -507,7 +516,7 @@ cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
   void* args[] = {&cc, &p, &fwd_pushed};
-  return cudaLaunchKernel(f, dim3(c.N), dim3(RT_THREADS), args, smem, s);
+  return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), smem, s, args);
 }
 
 cudaError_t launch_route(const DevCtx& c, int p, const int* next_ids, int n_next, size_t smem, cudaStream_t s) {
@@ -515,7 +524,7 @@ cudaError_t launch_route(const DevCtx& c, int p, const int* next_ids, int n_next
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
   void* args[] = {&cc, &p, &next_ids, &n_next};
-  return cudaLaunchKernel(f, dim3(c.N), dim3(RT_THREADS), args, smem, s);
+  return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), smem, s, args);
 }
 
 }  // namespace emb
