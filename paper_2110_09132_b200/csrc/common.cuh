@@ -75,6 +75,7 @@ struct DevCtx {
   int* long_slots;        // [2][N][max_long]   slots with more than one chunk
   int* counts;            // [2][N][CNT_W]      T, u, p, nchunks, nlong
   float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
+  int* slot_ctr;          // [2][N][max_tok]    chunk arrivals of multi-chunk slots (re-armed to 0)
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
   unsigned int* t_rec;    // [2]   t of the iteration using parity p

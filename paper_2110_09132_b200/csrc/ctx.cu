@@ -241,6 +241,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
     ALLOC(c.chunk_slot, 2 * N * (size_t)pl.max_chunks * 4);
     ALLOC(c.long_slots, 2 * N * (size_t)pl.max_long * 4);
+    ALLOC(c.slot_ctr, 2 * N * T * 4);
     ALLOC(c.counts, 2 * N * CNT_W * 4);
     ALLOC(c.scratch, 2 * (size_t)pl.max_chunks * cfg->dim * 4);
     if (cfg->mode == EMB_BWD_SPLIT && N > 1) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
@@ -410,8 +411,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
-    CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
-    if (mode == EMB_BWD_SPLIT) {
+    // N == 1: the coalesce applied every row's update itself (one source = the
+    // merged gradient); there is nothing to exchange or merge, for either part.
+    if (ctx->pl.N > 1)
+      CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
+    if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) {
       // scheduled part: lowest-priority side stream, after the prior part
       CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));
       CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));

@@ -97,10 +97,11 @@ __device__ __forceinline__ void sum_partials(const float* base, int dw, int ncol
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < V * EPV; ++i) acc[i] = 0.f;
-  for (int q = q0; q < q1; q += 4) {
-    float4 buf[4][V][EPV / 4];
+  constexpr int PB = 16 / EPV;  // partial rows in flight: 64 registers of loads whatever the dtype
+  for (int q = q0; q < q1; q += PB) {
+    float4 buf[PB][V][EPV / 4];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr)
+    for (int rr = 0; rr < PB; ++rr)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int c16 = lane + 32 * v;
@@ -110,7 +111,7 @@ __device__ __forceinline__ void sum_partials(const float* base, int dw, int ncol
             buf[rr][v][x] = __ldcg(reinterpret_cast<const float4*>(base + (size_t)(q + rr) * dw + c16 * EPV) + x);
       }
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr)
+    for (int rr = 0; rr < PB; ++rr)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int c16 = lane + 32 * v;
@@ -150,75 +151,176 @@ __device__ __forceinline__ void emit_coal_row(const DevCtx& c, int p, int k, int
   }
 }
 
-// ------------------------------------------------------------------ sender coalesce
+// Fused sparse optimizer step on one 16-byte chunk (EPV elements, column chunk
+// c16 of the rank's slice) of shard row u; g = the merged (unscaled) gradient.
+// SGD: w -= lr*g; Adam (PyTorch SparseAdam form, step t folded into alpha_t):
+// m += (1-b1)(g-m); v += (1-b2)(g^2-v); w -= alpha_t m / (sqrt(v)+eps).
+template <int DT>
+__device__ __forceinline__ void update_chunk(const DevCtx& c, int u, int c16, const float* g, float alpha) {
+  constexpr int EPV = Vec<DT>::EPV;
+  char* wp = shard_of(c, c.r) + ((size_t)u * c.d * c.esz) + (size_t)c16 * 16;
+  float w[EPV];
+  Vec<DT>::unpack(ld16(wp), w);
+  if (c.optim == SGD) {
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) w[i] = w[i] - c.lr * (c.scale * g[i]);
+  } else {
+    float* mp = c.adam_m + (size_t)u * c.d + c16 * EPV;
+    float* vp = c.adam_v + (size_t)u * c.d + c16 * EPV;
+    const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
+#pragma unroll
+    for (int i = 0; i < EPV; i += 4) {
+      const float4 m4 = *reinterpret_cast<const float4*>(mp + i);
+      const float4 v4 = *reinterpret_cast<const float4*>(vp + i);
+      float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float gs = c.scale * g[i + j];
+        mm[j] = mm[j] + om_b1 * (gs - mm[j]);
+        vv[j] = vv[j] + om_b2 * (gs * gs - vv[j]);
+        w[i + j] = w[i + j] - alpha * mm[j] / (sqrtf(vv[j]) + c.eps);
+      }
+      *reinterpret_cast<float4*>(mp + i) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+      *reinterpret_cast<float4*>(vp + i) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    }
+  }
+  st16(wp, Vec<DT>::pack(w));
+}
+
+// Emit the coalesced row of slot k.  N == 1: the coalesced row IS the merged
+// gradient of its id (a single source), so the optimizer step is applied right
+// here (no receive round trip, no merge kernel).  N > 1: round to the wire
+// dtype (the COAL/SPLIT rounding point, reading R11) and store into the
+// owners' receive rows (prior) or the stage (scheduled).
 template <int DT, int V>
-__global__ void __launch_bounds__(BWD_THREADS) coal_a_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+__device__ __forceinline__ void emit_slot(const DevCtx& c, int p, int k, int Pr, const float* acc, float alpha,
+                                          float* wsm /* this warp's D-float shared row */) {
+  constexpr int EPV = Vec<DT>::EPV;
+  const int lane = threadIdx.x & 31;
+  if (c.N == 1) {
+    // park the row in shared memory so the update loop below need not keep
+    // the accumulators live (register pressure)
+    store_partial<EPV, V>(wsm, c.cpr, acc);
+    __syncwarp();
+    const int u = c.slot_id[pn(c, p, c.r) * (size_t)c.max_tok + k];
+#pragma unroll 1
+    for (int c16 = lane; c16 < c.cpr; c16 += 32) {
+      float g[EPV];
+#pragma unroll
+      for (int x = 0; x < EPV; x += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(wsm + c16 * EPV + x);
+        g[x] = q.x; g[x + 1] = q.y; g[x + 2] = q.z; g[x + 3] = q.w;
+      }
+      // round to the wire dtype first: same rounding point as N > 1 (reading R11)
+      Vec<DT>::unpack(Vec<DT>::pack(g), g);
+      update_chunk<DT>(c, u, c16, g, alpha);
+    }
+    __syncwarp();
+    return;
+  }
+  emit_coal_row<DT, V>(c, p, k, Pr, acc);
+}
+
+// ------------------------------------------------------------------ sender coalesce
+// CTA b takes 8 consecutive chunks per round (one per warp).  Single-chunk
+// slots are emitted by their warp.  Chunks of multi-chunk (Zipf-head) slots
+// leave fp32 partials; after the round the CTA adds its chunk count to the
+// slot's arrival counter and the CTA completing a slot combines all of its
+// partials (warps sum contiguous partial ranges, then a fixed-order shared-
+// memory combine — deterministic whichever CTA arrives last) and emits it.
+template <int DT, int V>
+#ifndef EMB_COAL_MINB
+#define EMB_COAL_MINB 1  // CTAs per SM the register allocation must allow (A/B-tested)
+#endif
+__global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx c, const char* __restrict__ dY, int p) {
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
+  extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][D]
+  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
   const int* cnt = counts_of(c, p, r);
   const int U = cnt[CNT_U], Pr = cnt[CNT_P], NCH = cnt[CNT_NCH];
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int s = 0; s < c.N; ++s)
       atomicAdd(&c.stats[c.N + s], (unsigned long long)(c.N == 1 ? U : Pr) * c.d * c.esz);
+  const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;
   const size_t bpn = pn(c, p, r) * (size_t)c.max_tok;
   const int* perm = c.perm + bpn;
   const int* seg_start = c.seg_start + bpn;
   const int* seg_end = c.seg_end + bpn;
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
   const int* chunk_slot = c.chunk_slot + pn(c, p, r) * (size_t)c.max_chunks;
+  int* slot_ctr = c.slot_ctr + bpn;
+  float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
   const size_t row_bytes = (size_t)c.D * c.esz;
   float acc[V * EPV];
-  for (int ch = gw; ch < NCH; ch += nw) {
-    const int k = chunk_slot[ch];
-    const int c0 = chunk_off[k], nch = chunk_off[k + 1] - c0;
-    const int b = seg_start[k] + (ch - c0) * c.C;
-    const int e = min(seg_end[k], b + c.C);
-    reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
-    if (nch > 1) {
-      store_partial<EPV, V>(c.scratch + ((size_t)p * c.max_chunks + ch) * c.D, c.cpr, acc);
-    } else {
-      emit_coal_row<DT, V>(c, p, k, Pr, acc);
+  for (int base = blockIdx.x * BWD_WARPS; base < NCH; base += gridDim.x * BWD_WARPS) {
+    const int ch = base + w;
+    int k = -1, nch = 0;
+    if (ch < NCH) {
+      k = chunk_slot[ch];
+      const int c0 = chunk_off[k];
+      nch = chunk_off[k + 1] - c0;
+      const int b = seg_start[k] + (ch - c0) * c.C;
+      const int e = min(seg_end[k], b + c.C);
+      reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
+      if (nch > 1) store_partial<EPV, V>(part + (size_t)ch * c.D, c.cpr, acc);
+      else emit_slot<DT, V>(c, p, k, Pr, acc, alpha, wpart + (size_t)w * c.D);
     }
-  }
-  pdl_trigger();
-}
-
-template <int DT, int V>
-__global__ void __launch_bounds__(BWD_THREADS) coal_b_kernel(DevCtx c, int p) {
-  pdl_wait();
-  constexpr int EPV = Vec<DT>::EPV;
-  extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][D]
-  const int r = c.r;
-  const int* cnt = counts_of(c, p, r);
-  const int Pr = cnt[CNT_P], NL = cnt[CNT_NLONG];
-  const int* long_slots = c.long_slots + pn(c, p, r) * (size_t)c.max_long;
-  const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float acc[V * EPV];
-  for (int li = blockIdx.x; li < NL; li += gridDim.x) {
-    const int k = long_slots[li];
-    const int c0 = chunk_off[k], nch = chunk_off[k + 1] - c0;
-    const int q0 = c0 + (int)((long long)nch * w / BWD_WARPS), q1 = c0 + (int)((long long)nch * (w + 1) / BWD_WARPS);
-    sum_partials<EPV, V>(c.scratch + (size_t)p * c.max_chunks * c.D, c.D, c.cpr, q0, q1, acc);
-    store_partial<EPV, V>(wpart + (size_t)w * c.D, c.cpr, acc);
+    if (lane == 0) {
+      s_k[w] = (nch > 1) ? k : -1;
+      s_last[w] = -1;
+    }
     __syncthreads();
-    if (w == 0) {
-#pragma unroll
-      for (int i = 0; i < V * EPV; ++i) acc[i] = 0.f;
-      for (int ww = 0; ww < BWD_WARPS; ++ww)  // fixed order
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int c16 = lane + 32 * v;
-          if (c16 < c.cpr)
-#pragma unroll
-            for (int i = 0; i < EPV; ++i) acc[v * EPV + i] += wpart[(size_t)ww * c.D + c16 * EPV + i];
+    if (threadIdx.x == 0) {
+      // distinct multi-chunk slots of this round (their chunks are consecutive)
+      int nd = 0;
+      for (int i = 0; i < BWD_WARPS; ++i) {
+        if (s_k[i] < 0) continue;
+        if (nd > 0 && s_k[i] == s_last[nd - 1]) { s_n[nd - 1]++; continue; }
+        s_last[nd] = s_k[i];
+        s_n[nd] = 1;
+        ++nd;
+      }
+      __threadfence();  // this round's partials before the arrival counts
+      for (int i = 0; i < nd; ++i) {
+        const int kk = s_last[i];
+        const int tot = chunk_off[kk + 1] - chunk_off[kk];
+        const int prev = atomicAdd(&slot_ctr[kk], s_n[i]);
+        if (prev + s_n[i] == tot) {
+          slot_ctr[kk] = 0;  // re-arm (stream-ordered reuse next iteration of this parity)
+        } else {
+          s_last[i] = -1;    // not complete yet: another CTA will combine it
         }
-      emit_coal_row<DT, V>(c, p, k, Pr, acc);
+      }
+      for (int i = nd; i < BWD_WARPS; ++i) s_last[i] = -1;
+      __threadfence();
     }
     __syncthreads();
+    for (int i = 0; i < BWD_WARPS; ++i) {
+      const int kk = s_last[i];
+      if (kk < 0) continue;
+      const int c0 = chunk_off[kk], n2 = chunk_off[kk + 1] - c0;
+      const int q0 = c0 + (int)((long long)n2 * w / BWD_WARPS), q1 = c0 + (int)((long long)n2 * (w + 1) / BWD_WARPS);
+      sum_partials<EPV, V>(part, c.D, c.cpr, q0, q1, acc);
+      store_partial<EPV, V>(wpart + (size_t)w * c.D, c.cpr, acc);
+      __syncthreads();
+      if (w == 0) {
+#pragma unroll
+        for (int x = 0; x < V * EPV; ++x) acc[x] = 0.f;
+        for (int ww = 0; ww < BWD_WARPS; ++ww)  // fixed order
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int c16 = lane + 32 * v;
+            if (c16 < c.cpr)
+#pragma unroll
+              for (int x = 0; x < EPV; ++x) acc[v * EPV + x] += wpart[(size_t)ww * c.D + c16 * EPV + x];
+          }
+        emit_slot<DT, V>(c, p, kk, Pr, acc, alpha, wpart);
+      }
+      __syncthreads();
+    }
   }
   pdl_trigger();
 }
@@ -482,24 +584,21 @@ static int grid_for_warps(long long warps, int cap) {
                : cudaErrorInvalidValue)
 
 template <int DT>
-static void coal_b_smem(int V, size_t smem) {
+static void coal_smem(int V, size_t smem) {
   const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if (V <= 1) cudaFuncSetAttribute(coal_b_kernel<DT, 1>, a, (int)smem);
-  else if (V <= 2) cudaFuncSetAttribute(coal_b_kernel<DT, 2>, a, (int)smem);
-  else if (V <= 4) cudaFuncSetAttribute(coal_b_kernel<DT, 4>, a, (int)smem);
-  else cudaFuncSetAttribute(coal_b_kernel<DT, 8>, a, (int)smem);
+  if (V <= 1) cudaFuncSetAttribute(coal_kernel<DT, 1>, a, (int)smem);
+  else if (V <= 2) cudaFuncSetAttribute(coal_kernel<DT, 2>, a, (int)smem);
+  else if (V <= 4) cudaFuncSetAttribute(coal_kernel<DT, 4>, a, (int)smem);
+  else cudaFuncSetAttribute(coal_kernel<DT, 8>, a, (int)smem);
 }
 
 template <int DT>
 static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
   const int V = (c.cpr + 31) / 32;
   const int ga = grid_for_warps(c.max_chunks, L.nsm * 8);
-  cudaError_t e = EMB_LAUNCH_V(V, coal_a_kernel, DT, ga, 0, c, y, p);
-  if (e != cudaSuccess) return e;
   const size_t smem = (size_t)BWD_WARPS * c.D * 4;
-  const int gb = c.max_long < 1 ? 1 : c.max_long;
-  if (smem > 48 * 1024) coal_b_smem<DT>(V, smem);
-  return EMB_LAUNCH_V(V, coal_b_kernel, DT, gb, smem, c, p);
+  if (smem > 48 * 1024) coal_smem<DT>(V, smem);
+  return EMB_LAUNCH_V(V, coal_kernel, DT, ga, smem, c, y, p);
 }
 
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s) {
