@@ -33,21 +33,29 @@ namespace emb {
 static constexpr int BWD_THREADS = 256;
 static constexpr int BWD_WARPS = BWD_THREADS / 32;
 
+// Rows in flight per warp in the segmented reduce.  Most slots have 1-2 rows
+// (Zipf tail), so 2 in flight costs little latency and halves the load
+// registers (occupancy: 2 CTAs / SM without spills).
+#ifndef EMB_RB
+#define EMB_RB 2
+#endif
+
 // acc[v*EPV + i] = sum over rows perm[b..e) (ascending) of row[c16 = lane + 32 v]
 template <int DT, int V, bool PEER>
 __device__ __forceinline__ void reduce_rows(const char* __restrict__ base, size_t stride, int ncol16,
                                             const int* __restrict__ perm, int b, int e, float* acc) {
   constexpr int EPV = Vec<DT>::EPV;
+  constexpr int RB = EMB_RB;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < V * EPV; ++i) acc[i] = 0.f;
-  for (int i = b; i < e; i += 4) {
-    int pos[4];
+  for (int i = b; i < e; i += RB) {
+    int pos[RB];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) pos[rr] = (i + rr < e) ? __ldg(perm + i + rr) : 0;
-    uint4 buf[4][V];
+    for (int rr = 0; rr < RB; ++rr) pos[rr] = (i + rr < e) ? __ldg(perm + i + rr) : 0;
+    uint4 buf[RB][V];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
+    for (int rr = 0; rr < RB; ++rr) {
       if (i + rr < e) {
         const char* row = base + (size_t)pos[rr] * stride;
 #pragma unroll
@@ -58,7 +66,7 @@ __device__ __forceinline__ void reduce_rows(const char* __restrict__ base, size_
       }
     }
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
+    for (int rr = 0; rr < RB; ++rr) {
       if (i + rr < e) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -97,7 +105,7 @@ __device__ __forceinline__ void sum_partials(const float* base, int dw, int ncol
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < V * EPV; ++i) acc[i] = 0.f;
-  constexpr int PB = 16 / EPV;  // partial rows in flight: 64 registers of loads whatever the dtype
+  constexpr int PB = 8 / EPV;  // partial rows in flight: 32 registers of loads whatever the dtype
   for (int q = q0; q < q1; q += PB) {
     float4 buf[PB][V][EPV / 4];
 #pragma unroll
@@ -151,92 +159,152 @@ __device__ __forceinline__ void emit_coal_row(const DevCtx& c, int p, int k, int
   }
 }
 
-// Fused sparse optimizer step on one 16-byte chunk (EPV elements, column chunk
-// c16 of the rank's slice) of shard row u; g = the merged (unscaled) gradient.
-// SGD: w -= lr*g; Adam (PyTorch SparseAdam form, step t folded into alpha_t):
-// m += (1-b1)(g-m); v += (1-b2)(g^2-v); w -= alpha_t m / (sqrt(v)+eps).
-template <int DT>
-__device__ __forceinline__ void update_chunk(const DevCtx& c, int u, int c16, const float* g, float alpha) {
-  constexpr int EPV = Vec<DT>::EPV;
-  char* wp = shard_of(c, c.r) + ((size_t)u * c.d * c.esz) + (size_t)c16 * 16;
-  float w[EPV];
-  Vec<DT>::unpack(ld16(wp), w);
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Sparse optimizer math on EPV elements of one row chunk; g = merged, unscaled
+// gradient.  SGD: w -= lr*g.  Adam (PyTorch SparseAdam form, step t folded
+// into alpha_t, readings R3/R4): m += (1-b1)(g-m); v += (1-b2)(g^2-v);
+// w -= alpha_t m / (sqrt(v)+eps).  sqrt / reciprocal use the SFU (MUFU)
+// approximations: relative error ~1e-7, far inside the 1e-5 parity bound,
+// and an IEEE div+sqrt would be ~30 instructions per element.
+template <int EPV>
+__device__ __forceinline__ void opt_math(const DevCtx& c, float alpha, const float* g, float* w, float* mm, float* vv) {
   if (c.optim == SGD) {
 #pragma unroll
     for (int i = 0; i < EPV; ++i) w[i] = w[i] - c.lr * (c.scale * g[i]);
-  } else {
-    float* mp = c.adam_m + (size_t)u * c.d + c16 * EPV;
-    float* vp = c.adam_v + (size_t)u * c.d + c16 * EPV;
-    const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
-#pragma unroll
-    for (int i = 0; i < EPV; i += 4) {
-      const float4 m4 = *reinterpret_cast<const float4*>(mp + i);
-      const float4 v4 = *reinterpret_cast<const float4*>(vp + i);
-      float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float gs = c.scale * g[i + j];
-        mm[j] = mm[j] + om_b1 * (gs - mm[j]);
-        vv[j] = vv[j] + om_b2 * (gs * gs - vv[j]);
-        w[i + j] = w[i + j] - alpha * mm[j] / (sqrtf(vv[j]) + c.eps);
-      }
-      *reinterpret_cast<float4*>(mp + i) = make_float4(mm[0], mm[1], mm[2], mm[3]);
-      *reinterpret_cast<float4*>(vp + i) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-    }
-  }
-  st16(wp, Vec<DT>::pack(w));
-}
-
-// Emit the coalesced row of slot k.  N == 1: the coalesced row IS the merged
-// gradient of its id (a single source), so the optimizer step is applied right
-// here (no receive round trip, no merge kernel).  N > 1: round to the wire
-// dtype (the COAL/SPLIT rounding point, reading R11) and store into the
-// owners' receive rows (prior) or the stage (scheduled).
-template <int DT, int V>
-__device__ __forceinline__ void emit_slot(const DevCtx& c, int p, int k, int Pr, const float* acc, float alpha,
-                                          float* wsm /* this warp's D-float shared row */) {
-  constexpr int EPV = Vec<DT>::EPV;
-  const int lane = threadIdx.x & 31;
-  if (c.N == 1) {
-    // park the row in shared memory so the update loop below need not keep
-    // the accumulators live (register pressure)
-    store_partial<EPV, V>(wsm, c.cpr, acc);
-    __syncwarp();
-    const int u = c.slot_id[pn(c, p, c.r) * (size_t)c.max_tok + k];
-#pragma unroll 1
-    for (int c16 = lane; c16 < c.cpr; c16 += 32) {
-      float g[EPV];
-#pragma unroll
-      for (int x = 0; x < EPV; x += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(wsm + c16 * EPV + x);
-        g[x] = q.x; g[x + 1] = q.y; g[x + 2] = q.z; g[x + 3] = q.w;
-      }
-      // round to the wire dtype first: same rounding point as N > 1 (reading R11)
-      Vec<DT>::unpack(Vec<DT>::pack(g), g);
-      update_chunk<DT>(c, u, c16, g, alpha);
-    }
-    __syncwarp();
     return;
   }
-  emit_coal_row<DT, V>(c, p, k, Pr, acc);
+  const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
+#pragma unroll
+  for (int i = 0; i < EPV; ++i) {
+    const float gs = c.scale * g[i];
+    mm[i] = mm[i] + om_b1 * (gs - mm[i]);
+    vv[i] = vv[i] + om_b2 * (gs * gs - vv[i]);
+    w[i] = w[i] - alpha * mm[i] * rcp_approx(sqrt_approx(vv[i]) + c.eps);
+  }
+}
+
+// CTA-cooperative emission of coalesced rows parked in shared memory: row i
+// (D floats at rows + i*D) is slot ks[i] (skipped if < 0), shard row us[i].
+//   N == 1: the coalesced row IS the merged gradient of its id (one source):
+//           the optimizer step is applied here (no receive round trip, no
+//           merge kernel).  The row is first rounded to the wire dtype — the
+//           same rounding point as N > 1 (reading R11).
+//   N > 1:  round to the wire dtype and store the column slices into the
+//           owners' receive rows (prior slots, NVLink) or the stage (scheduled).
+// Every thread handles EU (row, 16-byte chunk) items with all loads issued
+// before any use.
+template <int DT>
+__device__ __forceinline__ void emit_rows(const DevCtx& c, int p, int Pr, const float* rows, const int* ks,
+                                          const int* us, int nrows, float alpha) {
+  constexpr int EPV = Vec<DT>::EPV;
+#ifndef EMB_EU
+#define EMB_EU 8
+#endif
+  constexpr int EU = EMB_EU / EPV;  // (row, chunk) items in flight: 2 fp32 / 1 bf16
+  const int total = nrows * c.cpr;
+  const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
+  const bool adam = (c.optim == ADAM);
+  for (int b0 = threadIdx.x; b0 < total; b0 += blockDim.x * EU) {
+    int ii[EU], cc[EU];
+    bool ok[EU];
+#pragma unroll
+    for (int j = 0; j < EU; ++j) {
+      const int it = b0 + j * blockDim.x;
+      ii[j] = it / c.cpr;
+      cc[j] = it - ii[j] * c.cpr;
+      ok[j] = it < total && ks[ii[j]] >= 0;
+    }
+    if (c.N == 1) {
+      uint4 wr[EU];
+      float mm[EU][EPV], vv[EU][EPV];
+#pragma unroll
+      for (int j = 0; j < EU; ++j) {
+        if (!ok[j]) continue;
+        const size_t u = (size_t)us[ii[j]];
+        wr[j] = ld16(shard_of(c, c.r) + u * slice_bytes + (size_t)cc[j] * 16);
+        if (adam) {
+#pragma unroll
+          for (int x = 0; x < EPV; x += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + cc[j] * EPV + x);
+            const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + cc[j] * EPV + x);
+            mm[j][x] = m4.x; mm[j][x + 1] = m4.y; mm[j][x + 2] = m4.z; mm[j][x + 3] = m4.w;
+            vv[j][x] = v4.x; vv[j][x + 1] = v4.y; vv[j][x + 2] = v4.z; vv[j][x + 3] = v4.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < EU; ++j) {
+        if (!ok[j]) continue;
+        const size_t u = (size_t)us[ii[j]];
+        float g[EPV], w[EPV];
+        const float* src = rows + (size_t)ii[j] * c.D + cc[j] * EPV;
+#pragma unroll
+        for (int x = 0; x < EPV; ++x) g[x] = src[x];
+        Vec<DT>::unpack(Vec<DT>::pack(g), g);  // wire rounding point
+        Vec<DT>::unpack(wr[j], w);
+        opt_math<EPV>(c, alpha, g, w, mm[j], vv[j]);
+        st16(shard_of(c, c.r) + u * slice_bytes + (size_t)cc[j] * 16, Vec<DT>::pack(w));
+        if (adam) {
+#pragma unroll
+          for (int x = 0; x < EPV; x += 4) {
+            *reinterpret_cast<float4*>(c.adam_m + u * c.d + cc[j] * EPV + x) =
+                make_float4(mm[j][x], mm[j][x + 1], mm[j][x + 2], mm[j][x + 3]);
+            *reinterpret_cast<float4*>(c.adam_v + u * c.d + cc[j] * EPV + x) =
+                make_float4(vv[j][x], vv[j][x + 1], vv[j][x + 2], vv[j][x + 3]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < EU; ++j) {
+        if (!ok[j]) continue;
+        const int k = ks[ii[j]], c16 = cc[j];
+        float g[EPV];
+        const float* src = rows + (size_t)ii[j] * c.D + c16 * EPV;
+#pragma unroll
+        for (int x = 0; x < EPV; ++x) g[x] = src[x];
+        const uint4 val = Vec<DT>::pack(g);
+        if (k < Pr) {
+          const int s = c16 / c.cps, cs = c16 - s * c.cps;
+          st16(recv_of(c, s, p, c.r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
+        } else {
+          st16(c.stage + ((size_t)p * c.max_tok + (k - Pr)) * row_bytes + (size_t)c16 * 16, val);
+        }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ sender coalesce
-// CTA b takes 8 consecutive chunks per round (one per warp).  Single-chunk
-// slots are emitted by their warp.  Chunks of multi-chunk (Zipf-head) slots
-// leave fp32 partials; after the round the CTA adds its chunk count to the
-// slot's arrival counter and the CTA completing a slot combines all of its
-// partials (warps sum contiguous partial ranges, then a fixed-order shared-
-// memory combine — deterministic whichever CTA arrives last) and emits it.
-template <int DT, int V>
+// CTA b takes 8 consecutive chunks per round (one per warp).  Each warp
+// reduces its chunk (<= C rows, ascending position, fp32).  A single-chunk
+// slot's row is parked in shared memory and the CTA emits the parked rows
+// together (emit_rows).  Chunks of multi-chunk (Zipf-head) slots leave fp32
+// partials; the CTA then adds its chunk count to the slot's arrival counter,
+// and the CTA completing a slot combines all of its partials (warps sum
+// contiguous partial ranges, then a fixed-order shared-memory combine —
+// deterministic whichever CTA arrives last) and emits it.
 #ifndef EMB_COAL_MINB
-#define EMB_COAL_MINB 1  // CTAs per SM the register allocation must allow (A/B-tested)
+#define EMB_COAL_MINB 1  // 2 forces 128 registers and spills: measured 1.7x slower (round 1)
 #endif
+template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx c, const char* __restrict__ dY, int p) {
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
-  extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][D]
-  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS];
+  extern __shared__ __align__(16) float smem_f[];
+  float* rows = smem_f;                        // [BWD_WARPS][D] parked single-chunk rows / combined row
+  float* comb = smem_f + BWD_WARPS * c.D;      // [BWD_WARPS][D] warp partials of a long slot
+  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS], s_ks[BWD_WARPS], s_us[BWD_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
   const int* cnt = counts_of(c, p, r);
@@ -249,27 +317,31 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
   const int* perm = c.perm + bpn;
   const int* seg_start = c.seg_start + bpn;
   const int* seg_end = c.seg_end + bpn;
+  const int* slot_id = c.slot_id + bpn;
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
   const int* chunk_slot = c.chunk_slot + pn(c, p, r) * (size_t)c.max_chunks;
   int* slot_ctr = c.slot_ctr + bpn;
   float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
   const size_t row_bytes = (size_t)c.D * c.esz;
-  float acc[V * EPV];
   for (int base = blockIdx.x * BWD_WARPS; base < NCH; base += gridDim.x * BWD_WARPS) {
     const int ch = base + w;
     int k = -1, nch = 0;
-    if (ch < NCH) {
-      k = chunk_slot[ch];
-      const int c0 = chunk_off[k];
-      nch = chunk_off[k + 1] - c0;
-      const int b = seg_start[k] + (ch - c0) * c.C;
-      const int e = min(seg_end[k], b + c.C);
-      reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
-      if (nch > 1) store_partial<EPV, V>(part + (size_t)ch * c.D, c.cpr, acc);
-      else emit_slot<DT, V>(c, p, k, Pr, acc, alpha, wpart + (size_t)w * c.D);
+    {
+      float acc[V * EPV];
+      if (ch < NCH) {
+        k = chunk_slot[ch];
+        const int c0 = chunk_off[k];
+        nch = chunk_off[k + 1] - c0;
+        const int b = seg_start[k] + (ch - c0) * c.C;
+        const int e = min(seg_end[k], b + c.C);
+        reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
+        store_partial<EPV, V>((nch > 1) ? part + (size_t)ch * c.D : rows + (size_t)w * c.D, c.cpr, acc);
+      }
     }
     if (lane == 0) {
       s_k[w] = (nch > 1) ? k : -1;
+      s_ks[w] = (ch < NCH && nch == 1) ? k : -1;
+      s_us[w] = (ch < NCH && nch == 1 && c.N == 1) ? slot_id[k] : 0;
       s_last[w] = -1;
     }
     __syncthreads();
@@ -288,37 +360,38 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
         const int kk = s_last[i];
         const int tot = chunk_off[kk + 1] - chunk_off[kk];
         const int prev = atomicAdd(&slot_ctr[kk], s_n[i]);
-        if (prev + s_n[i] == tot) {
-          slot_ctr[kk] = 0;  // re-arm (stream-ordered reuse next iteration of this parity)
-        } else {
-          s_last[i] = -1;    // not complete yet: another CTA will combine it
-        }
+        if (prev + s_n[i] == tot) slot_ctr[kk] = 0;  // complete here; re-arm for the next use
+        else s_last[i] = -1;                          // another CTA will combine it
       }
       for (int i = nd; i < BWD_WARPS; ++i) s_last[i] = -1;
       __threadfence();
     }
+    __syncthreads();
+    emit_rows<DT>(c, p, Pr, rows, s_ks, s_us, BWD_WARPS, alpha);
     __syncthreads();
     for (int i = 0; i < BWD_WARPS; ++i) {
       const int kk = s_last[i];
       if (kk < 0) continue;
       const int c0 = chunk_off[kk], n2 = chunk_off[kk + 1] - c0;
       const int q0 = c0 + (int)((long long)n2 * w / BWD_WARPS), q1 = c0 + (int)((long long)n2 * (w + 1) / BWD_WARPS);
-      sum_partials<EPV, V>(part, c.D, c.cpr, q0, q1, acc);
-      store_partial<EPV, V>(wpart + (size_t)w * c.D, c.cpr, acc);
-      __syncthreads();
-      if (w == 0) {
-#pragma unroll
-        for (int x = 0; x < V * EPV; ++x) acc[x] = 0.f;
-        for (int ww = 0; ww < BWD_WARPS; ++ww)  // fixed order
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const int c16 = lane + 32 * v;
-            if (c16 < c.cpr)
-#pragma unroll
-              for (int x = 0; x < EPV; ++x) acc[v * EPV + x] += wpart[(size_t)ww * c.D + c16 * EPV + x];
-          }
-        emit_slot<DT, V>(c, p, kk, Pr, acc, alpha, wpart);
+      {
+        float acc[V * EPV];
+        sum_partials<EPV, V>(part, c.D, c.cpr, q0, q1, acc);
+        store_partial<EPV, V>(comb + (size_t)w * c.D, c.cpr, acc);
       }
+      __syncthreads();
+      for (int x = threadIdx.x; x < c.D; x += blockDim.x) {  // fixed warp order
+        float sum = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < BWD_WARPS; ++ww) sum += comb[(size_t)ww * c.D + x];
+        rows[x] = sum;
+      }
+      if (threadIdx.x == 0) {
+        s_ks[0] = kk;
+        s_us[0] = (c.N == 1) ? slot_id[kk] : 0;
+      }
+      __syncthreads();
+      emit_rows<DT>(c, p, Pr, rows, s_ks, s_us, 1, alpha);
       __syncthreads();
     }
   }
@@ -596,7 +669,7 @@ template <int DT>
 static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
   const int V = (c.cpr + 31) / 32;
   const int ga = grid_for_warps(c.max_chunks, L.nsm * 8);
-  const size_t smem = (size_t)BWD_WARPS * c.D * 4;
+  const size_t smem = (size_t)2 * BWD_WARPS * c.D * 4;
   if (smem > 48 * 1024) coal_smem<DT>(V, smem);
   return EMB_LAUNCH_V(V, coal_kernel, DT, ga, smem, c, y, p);
 }
