@@ -144,25 +144,31 @@ def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
     # forward: Y write + distinct rows read (every owner's slice) + ids; NVLink in = (N-1)/N of rows
     out["fwd_pull_gather"] = (T[rank] * cfg.D * esz + u_fwd * cfg.D * esz + T[rank] * 4,
                               (N - 1) * T[rank] * d * esz)
-    out["ids_push_mark"] = (sum(T) * 4 + T[rank] * 4 * N + (sum(T) * 4 if mode == "split" else 0),
-                            (N - 1) * T[rank] * 4)
-    out["route_sort_split"] = (sum(T) * 4 * 2 + sum(u) * 4 * 4 + sum(u) * 8, 0)
-    c_r = T[rank] if mode == "raw" else u[rank]
+    # a5 prefetch push (+ D_next marks in SPLIT); a6 sort (aux stream); a8 tables (aux)
+    out["mark_next"] = (T[rank] * 4 * (N + 1) + (sum(T) * 8 if mode == "split" else 0), (N - 1) * T[rank] * 4)
+    out["sort_unique"] = (sum(T) * 4 * 3 + sum(u) * 4 * 4 + (sum(u) * 8 if N > 1 else 0), 0)
+    out["split_tables"] = (sum(u) * 4 * 3, 0)
+    opt_b = 16 if cfg.optim == "adam" else 0   # Adam m, v fp32: read + write
+    row_state = 2 * esz + opt_b               # shard row element read + write (+ m, v)
     if mode == "raw":
         out["rawpush"] = (T[rank] * cfg.D * esz * 2, (N - 1) * T[rank] * d * esz)
         out["rawcoal"] = (sum(T) * d * esz + sum(u) * d * 4, 0)
         src = 4
+    elif N == 1:
+        # dY read once + the optimizer step applied in the coalesce (no exchange, no merge)
+        out["coal_push"] = (T[rank] * cfg.D * esz + Uall.size * cfg.D * row_state, 0)
+        return out
     else:
+        c_r = u[rank]
         out["coal_push"] = (T[rank] * cfg.D * esz + c_r * cfg.D * esz, (N - 1) * c_r * d * esz)
         src = esz
-    opt_b = 16 if cfg.optim == "adam" else 0
     frac_p = (P / Uall.size) if Uall.size else 0
     contrib = sum(u) * d * src
-    out["merge_update_prior"] = (int(frac_p * contrib) + P * d * (2 * esz + opt_b), 0)
+    out["merge_update_prior"] = (int(frac_p * contrib) + P * d * row_state, 0)
     if mode == "split":
         q_r = len(np.setdiff1d(U_n[rank], nxt))
         out["defpush"] = (2 * q_r * cfg.D * esz, (N - 1) * q_r * d * esz)
-        out["merge_update_sched"] = (int((1 - frac_p) * contrib) + Q * d * (2 * esz + opt_b), 0)
+        out["merge_update_sched"] = (int((1 - frac_p) * contrib) + Q * d * row_state, 0)
     return out
 
 

@@ -112,14 +112,15 @@ typedef struct {
 typedef enum {
   EMB_K_FWD = 0,      /* a1-a4 forward pull-gather (+ id all-gather push)        */
   EMB_K_SORT = 1,     /* a6 per-source sort / unique (auxiliary stream)           */
-  EMB_K_ROUTE = 2,    /* a5 + a8 next-id push, D_next, Alg. 1 split, chunks       */
+  EMB_K_ROUTE = 2,    /* a5 next-id push (prefetch all-gather) + D_next marks     */
   EMB_K_COAL = 3,     /* a7 + a9 + a10 sender coalesce + prior push               */
   EMB_K_MERGE0 = 4,   /* a11 owner merge + update, prior (or whole) part          */
   EMB_K_DEFPUSH = 5,  /* a12 scheduled rows push                                  */
   EMB_K_MERGE1 = 6,   /* a12 owner merge + update, scheduled part                 */
   EMB_K_RAWPUSH = 7,  /* RAW a10 raw slice push                                   */
   EMB_K_RAWCOAL = 8,  /* RAW owner-side coalesce                                  */
-  EMB_NUM_KERNELS = 9
+  EMB_K_TABLES = 9,   /* a8 Alg. 1 slot tables P_n ++ D_n (off the critical path) */
+  EMB_NUM_KERNELS = 10
 } emb_kernel_kind;
 
 /* Debug items for emb_debug_copy (integer parity tests). `src` selects the

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #define EMB_WMAX 8
@@ -14,10 +15,10 @@ enum Mode { RAW = 0, COAL = 1, SPLIT = 2 };
 enum Optim { SGD = 0, ADAM = 1 };
 enum DType { F32 = 0, BF16 = 1 };
 enum ErrBit { ERR_ID = 1, ERR_STATE = 2, ERR_TIMEOUT = 4 };
-// counts[p][n][CNT_W]: T, u, p, nchunks, nlong are written by route and read
-// by the backward kernels; ST / SU are the sort's own copies (the sort of the
-// next batch may run while the scheduled merge still reads u / p).
-enum CountSlot { CNT_T = 0, CNT_U = 1, CNT_P = 2, CNT_NCH = 3, CNT_NLONG = 4, CNT_ST = 5, CNT_SU = 6, CNT_W = 8 };
+// counts[p][n][CNT_W]
+//   written by sort(t):   T, U (unique kept ids), NCH (reduce chunks), NLONG (multi-chunk uniques)
+//   written by tables(t): P (prior uniques of the Alg. 1 split; stats / debug only)
+enum CountSlot { CNT_T = 0, CNT_U = 1, CNT_P = 2, CNT_NCH = 3, CNT_NLONG = 4, CNT_W = 8 };
 
 // Peer-written flags living in every rank's NVLink-visible region.  Slot [n]
 // is written only by rank n (epoch values = iteration number t, monotone).
@@ -36,7 +37,8 @@ struct SymLayout {
   size_t shard;   // [L][d]             table dtype     (peers read: forward pull)
   size_t gids;    // [2][N][max_tok]    int32           (peers write: id all-gather)
   size_t ntok;    // [2][N]             int32
-  size_t recv;    // [2][N][max_tok][d] wire = table dtype (senders write: grad AlltoAll)
+  size_t recv;    // [2][N][max_tok][d] wire = table dtype (senders write: grad AlltoAll),
+                  //                    row i = sender's unique id i
   size_t flags;   // Flags
   size_t total;
 };
@@ -54,32 +56,31 @@ struct DevCtx {
   unsigned long long timeout_ns;
   int C;                  // rows per reduce chunk
   int max_chunks;         // per source per parity
-  int max_long;           // multi-chunk slots per source per parity (<= max_tok / (C+1) + 1)
+  int max_long;           // multi-chunk uniques per source per parity (<= max_tok / (C+1) + 1)
   int idbits, posbits;
 
   char* sym[EMB_WMAX];    // base of every rank's symmetric region (own included)
   SymLayout lay;
 
-  // local (not peer-visible)
+  // local (not peer-visible); [2] = iteration parity p = t & 1
   float* adam_m;          // [L][d]
   float* adam_v;          // [L][d]
-  unsigned long long* slotmap;  // [L][N] (t << 32) | slot — source n holds id in slot k at iteration t (N > 1)
+  int* nextmark;          // [2][L]   epoch tag: id in D_next of iteration v <=> nextmark[v&1][id] == v+1
+  unsigned long long* slotmap;  // [2][L][N] (t << 32) | i — source n holds id as unique i at iteration t (N > 1)
   int* perm;              // [2][N][max_tok]    positions sorted by (dropped, id, position)
-  int* uid;               // [2][N][max_tok]    ascending unique kept ids (sort output)
-  int* useg;              // [2][N][max_tok+1]  unique index -> first index into perm
-  int* slot_id;           // [2][N][max_tok]    slot k -> id
-  int* seg_start;         // [2][N][max_tok]    slot k -> first index into perm
-  int* seg_end;           // [2][N][max_tok]    slot k -> one past last
-  int* chunk_off;         // [2][N][max_tok+1]  slot k -> first chunk
-  int* chunk_slot;        // [2][N][max_chunks] chunk -> slot
-  int* long_slots;        // [2][N][max_long]   slots with more than one chunk
-  int* counts;            // [2][N][CNT_W]      T, u, p, nchunks, nlong
+  int* uid;               // [2][N][max_tok]    ascending unique kept ids
+  int* useg;              // [2][N][max_tok+1]  unique i -> first index into perm (useg[U] = end)
+  int* chunk_off;         // [2][N][max_tok+1]  unique i -> first reduce chunk
+  int* chunk_uidx;        // [2][N][max_chunks] chunk -> unique i
+  int* long_u;            // [2][N][max_long]   uniques with more than one chunk
+  int* slot_id;           // [2][N][max_tok]    Alg. 1 slot order (prior asc, then scheduled asc) — tables
+  int* counts;            // [2][N][CNT_W]
   float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
-  int* slot_ctr;          // [2][N][max_tok]    chunk arrivals of multi-chunk slots (re-armed to 0)
+  int* slot_ctr;          // [2][N][max_tok]    chunk arrivals of multi-chunk uniques (re-armed to 0)
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
-  float* alpha;           // [2]   Adam step size alpha_t of the iteration using parity p (route computes it once)
+  float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
   unsigned long long* dbg_ts; // [64] phase timestamps (EMB_PHASE_TIMING builds only)
@@ -114,6 +115,10 @@ __device__ __forceinline__ size_t pn(const DevCtx& c, int p, int n) { return (si
 __device__ __forceinline__ const int* counts_of(const DevCtx& c, int p, int n) {
   return c.counts + pn(c, p, n) * CNT_W;
 }
+// Alg. 1 class of an id in iteration t (parity p): prior iff in the gathered next batch
+__device__ __forceinline__ bool is_prior(const DevCtx& c, int p, uint32_t t, int id) {
+  return c.mode != SPLIT || __ldcg(c.nextmark + (size_t)p * c.L + id) == (int)(t + 1);
+}
 
 // ----------------------------------------------------------------- memory model
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -143,7 +148,6 @@ __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag,
   }
 }
 
-// Thread-level: wait for flags[s] >= target for every rank s.
 // N == 1: every producer/consumer pair is ordered by the stream or an event,
 // so the flag protocol (and its system fences) is skipped entirely.
 __device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target) {

@@ -64,8 +64,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   pl->posbits = bits_for(cfg->max_tokens - 1);
   pl->key64 = 1 + pl->idbits + pl->posbits > 32;  // dropped bit | id | pos
   pl->sort_smem = sort_smem_bytes(cfg->max_tokens, pl->key64);
-  pl->route_smem = route_smem_bytes(cfg->vocab);
-  if (pl->sort_smem > 227 * 1024 || pl->route_smem > 227 * 1024) return EMB_ERR_CAPACITY;
+  if (pl->sort_smem > 227 * 1024) return EMB_ERR_CAPACITY;
 
   const size_t L = (size_t)cfg->vocab, T = (size_t)cfg->max_tokens;
   SymLayout& y = pl->lay;
@@ -79,9 +78,11 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
 
   size_t loc = 0;
   if (cfg->optim == EMB_ADAM) loc += 2 * L * pl->d * 4;
-  if (N > 1) loc += L * N * 8;
-  loc += 4 * 2 * N * T * 4 + 2 * N * (T + 1) * 4 + 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * CNT_W * 4;
-  loc += 2 * N * (size_t)pl->max_long * 4 + 2 * (size_t)pl->max_chunks * cfg->dim * 4;
+  if (N > 1) loc += 2 * L * N * 8;                               // slotmap
+  loc += 2 * L * 4;                                              // nextmark
+  loc += 5 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id slot_ctr | useg chunk_off
+  loc += 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * CNT_W * 4 + 2 * N * (size_t)pl->max_long * 4;
+  loc += 2 * (size_t)pl->max_chunks * cfg->dim * 4;              // scratch
   if (cfg->mode == EMB_BWD_SPLIT && N > 1) loc += 2 * T * cfg->dim * pl->esz;
   if (cfg->mode == EMB_BWD_RAW) loc += 2 * N * T * pl->d * 4;
   pl->local_bytes = loc;
@@ -105,6 +106,9 @@ struct emb_ctx {
   cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
+  cudaEvent_t ev_marked = nullptr, ev_join_aux = nullptr, ev_join_side = nullptr;
+  bool mark_pending = false;  // N == 1: mark runs on aux; the next forward checks its pushed ids
+  bool aux_used = false, side_used = false;  // since the last emb_join
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
@@ -231,16 +235,15 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
       ALLOC(c.adam_m, L * pl.d * 4);
       ALLOC(c.adam_v, L * pl.d * 4);
     }
-    if (N > 1) ALLOC(c.slotmap, L * N * 8);
+    if (N > 1) ALLOC(c.slotmap, 2 * L * N * 8);
+    ALLOC(c.nextmark, 2 * L * 4);
     ALLOC(c.perm, 2 * N * T * 4);
     ALLOC(c.uid, 2 * N * T * 4);
     ALLOC(c.useg, 2 * N * (T + 1) * 4);
     ALLOC(c.slot_id, 2 * N * T * 4);
-    ALLOC(c.seg_start, 2 * N * T * 4);
-    ALLOC(c.seg_end, 2 * N * T * 4);
     ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
-    ALLOC(c.chunk_slot, 2 * N * (size_t)pl.max_chunks * 4);
-    ALLOC(c.long_slots, 2 * N * (size_t)pl.max_long * 4);
+    ALLOC(c.chunk_uidx, 2 * N * (size_t)pl.max_chunks * 4);
+    ALLOC(c.long_u, 2 * N * (size_t)pl.max_long * 4);
     ALLOC(c.slot_ctr, 2 * N * T * 4);
     ALLOC(c.counts, 2 * N * CNT_W * 4);
     ALLOC(c.scratch, 2 * (size_t)pl.max_chunks * cfg->dim * 4);
@@ -253,7 +256,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.dbg_ts, 64 * 8);
   }
 #undef ALLOC
-  if (route_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem, pl.route_smem) != cudaSuccess) goto fail;
+  if (sort_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem) != cudaSuccess) goto fail;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
@@ -266,6 +269,9 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cudaEventCreateWithFlags(&ctx->ev_main[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_sorted[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
   }
+  if (cudaEventCreateWithFlags(&ctx->ev_marked, cudaEventDisableTiming) != cudaSuccess) goto fail;
+  if (cudaEventCreateWithFlags(&ctx->ev_join_aux, cudaEventDisableTiming) != cudaSuccess) goto fail;
+  if (cudaEventCreateWithFlags(&ctx->ev_join_side, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
   *out = ctx;
   return EMB_OK;
@@ -355,6 +361,10 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->it += 1;
   const int p = (int)(ctx->it & 1);
   if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+  if (ctx->mark_pending) {  // N == 1: the prefetch push ran on the aux stream
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_marked, 0));
+    ctx->mark_pending = false;
+  }
   const int pre = ctx->prefetched ? 1 : 0;
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
   if (!pre) {
@@ -367,6 +377,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     }));
     CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], ctx->aux));
     ctx->sort_pending[p] = true;
+    ctx->aux_used = true;
   }
   ctx->prefetched = false;
   ctx->last_n = n;
@@ -390,20 +401,37 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   const int last_n = ctx->last_n;
   cudaStream_t side = ctx->side;
   cudaStream_t aux = ctx->aux;
-  if (ctx->sort_pending[p]) {  // the sort of this batch (aux stream) must be complete
-    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
-    ctx->sort_pending[p] = false;
+  const int N = ctx->pl.N;
+  const int do_mark = (mode == EMB_BWD_SPLIT && next_ids) ? 1 : 0;
+  // a5: prefetch all-gather of the next ids + D_next marks.  N > 1 the owners
+  // need the marks before the coalesce (prior rows travel first): main stream.
+  // N == 1 nothing on the critical path needs them (the coalesce applies every
+  // row; the split only feeds the tables): aux stream, overlapping the coalesce.
+  CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));  // caller's next_ids / dY are ready in stream order
+  cudaStream_t ms = (N > 1) ? stream : aux;
+  if (N == 1) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
+  CKC(ctx, run_k(ctx, EMB_K_ROUTE, ms, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, ms); }));
+  if (N == 1) {
+    CKC(ctx, cudaEventRecord(ctx->ev_marked, aux));
+    ctx->mark_pending = true;
+  } else {
+    CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
+    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
   }
-  CKC(ctx, run_k(ctx, EMB_K_ROUTE, stream,
-                 [&] { return launch_route(c, p, next_ids, n_next, ctx->pl.route_smem, stream); }));
+  ctx->aux_used = true;
+  // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
+  CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
   if (next_ids) {
-    // prefetch: route pushed the next batch's ids; sort them now, overlapping
-    // the rest of this iteration and the next forward
-    CKC(ctx, cudaEventRecord(ctx->ev_main[p ^ 1], stream));
-    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p ^ 1], 0));
+    // a6 for the next batch, one iteration ahead.  Its parity's previous user
+    // (the scheduled merge of t-1) must be done with the routing tables.
+    if (ctx->def_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_def[p ^ 1], 0));
     CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] { return launch_sort(c, p ^ 1, 0, ctx->pl.key64, ctx->pl.sort_smem, aux); }));
     CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
     ctx->sort_pending[p ^ 1] = true;
+  }
+  if (ctx->sort_pending[p]) {  // the sort of this batch (aux stream) must be complete
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
+    ctx->sort_pending[p] = false;
   }
   if (mode == EMB_BWD_RAW) {
     CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
@@ -424,6 +452,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, run_k(ctx, EMB_K_MERGE1, side, [&] { return launch_merge(c, lc, p, 1, side); }));
       CKC(ctx, cudaEventRecord(ctx->ev_def[p], ctx->side));
       ctx->def_pending[p] = true;
+      ctx->side_used = true;
     }
   }
   ctx->prefetched = next_ids != nullptr;
@@ -489,16 +518,22 @@ emb_status emb_join(emb_ctx* ctx, emb_stream_t stream_) {
   emb_status st = ctx_check(ctx);
   if (st != EMB_OK) return st;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-  for (int p = 0; p < 2; ++p) {
-    if (ctx->def_pending[p]) {
-      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
-      ctx->def_pending[p] = false;  // later work on `stream` is ordered after it
-    }
-    if (ctx->sort_pending[p]) {
-      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
-      ctx->sort_pending[p] = false;
-    }
+  // everything enqueued so far on the library's streams precedes later work on `stream`
+  if (ctx->aux_used) {
+    CKC(ctx, cudaEventRecord(ctx->ev_join_aux, ctx->aux));
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux, 0));
+    ctx->aux_used = false;
   }
+  if (ctx->side_used) {
+    CKC(ctx, cudaEventRecord(ctx->ev_join_side, ctx->side));
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_side, 0));
+    ctx->side_used = false;
+  }
+  for (int p = 0; p < 2; ++p) {
+    ctx->def_pending[p] = false;
+    ctx->sort_pending[p] = false;
+  }
+  ctx->mark_pending = false;
   return EMB_OK;
 }
 
@@ -653,6 +688,9 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_def[i]) cudaEventDestroy(ctx->ev_def[i]);
     if (ctx->ev_main[i]) cudaEventDestroy(ctx->ev_main[i]);
     if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
+  }
+  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side}) {
+    if (e) cudaEventDestroy(e);
   }
   delete ctx;
   return EMB_OK;

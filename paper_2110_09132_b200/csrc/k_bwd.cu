@@ -8,20 +8,24 @@
 // the scheduled part ("delayed", assigned "the latest" priority).
 // Modified Adam: one step value t for both parts (reading R3).
 //
-// B200 design:
-//   coal_a   sender-side segmented reduce of dY in fp32, one warp per chunk of
-//            <= C rows of a slot (4 rows in flight per warp).  Single-chunk
-//            slots (almost all) are rounded to the wire dtype and stored
-//            DIRECTLY into each owner's receive rows over NVLink (prior slots)
-//            or into a local stage (scheduled slots, N > 1) — COALESCE +
-//            INDEX_SELECT + AlltoAll in one pass.  Multi-chunk (Zipf-head)
-//            slots leave fp32 partials.
-//   coal_b   one CTA per multi-chunk slot: warps sum contiguous partial ranges,
-//            then a fixed-order shared-memory combine (deterministic, no float
-//            atomics), then the same emit.
+// B200 design.  Rows are addressed by the sender's
+// unique index i (ascending unique ids from the sort); the prior / scheduled
+// class of a row is the D_next mark of its id.
+//   coal     sender-side segmented reduce of dY in fp32, one warp per chunk of
+//            <= C rows (2 in flight), ascending positions; chunks of multi-
+//            chunk (Zipf-head) uniques leave fp32 partials that the CTA which
+//            completes the unique combines in a fixed order (deterministic, no
+//            float atomics).  Coalesced rows are parked in shared memory and
+//            emitted by the whole CTA:
+//              N == 1  optimizer step applied in place (one source = the
+//                      merged gradient: no exchange, no merge kernel);
+//              N > 1   rounded to the wire dtype and stored straight into each
+//                      owner's receive row i over NVLink (prior rows), or into
+//                      the local stage (scheduled rows) — COALESCE +
+//                      INDEX_SELECT + AlltoAll in one pass.
 //   defpush  pushes the staged scheduled rows (side stream, lowest priority).
-//   rawpush / rawcoal_a / rawcoal_b   RAW mode: raw dY slices travel, the
-//            owner coalesces every source (fp32, no wire rounding).
+//   rawpush / rawcoal   RAW mode: raw dY slices travel, the owner coalesces
+//            every source (fp32, no wire rounding).
 //   merge    owner: each row's contributions summed in ascending source rank
 //            (fp32), scaled, fused SGD / Adam update of shard, m, v.
 #include <stddef.h>
@@ -33,9 +37,8 @@ namespace emb {
 static constexpr int BWD_THREADS = 256;
 static constexpr int BWD_WARPS = BWD_THREADS / 32;
 
-// Rows in flight per warp in the segmented reduce.  Most slots have 1-2 rows
-// (Zipf tail), so 2 in flight costs little latency and halves the load
-// registers (occupancy: 2 CTAs / SM without spills).
+// Rows in flight per warp in the segmented reduce.  Most uniques have 1-2 rows
+// (Zipf tail), so 2 in flight costs little latency and saves load registers.
 #ifndef EMB_RB
 #define EMB_RB 2
 #endif
@@ -99,7 +102,7 @@ __device__ __forceinline__ void store_partial(float* dst, int ncol16, const floa
   }
 }
 
-// Sum partial rows [q0, q1) (ascending) into acc — 4 partial rows in flight.
+// Sum partial rows [q0, q1) (ascending) into acc.
 template <int EPV, int V>
 __device__ __forceinline__ void sum_partials(const float* base, int dw, int ncol16, int q0, int q1, float* acc) {
   const int lane = threadIdx.x & 31;
@@ -135,30 +138,6 @@ __device__ __forceinline__ void sum_partials(const float* base, int dw, int ncol
   }
 }
 
-// Emit sender slot k of this rank (coalesced row, wire dtype): prior slots (and
-// every slot when N == 1) go straight into owner s's receive row k; scheduled
-// slots (N > 1) go to the local stage for the side-stream push.
-template <int DT, int V>
-__device__ __forceinline__ void emit_coal_row(const DevCtx& c, int p, int k, int Pr, const float* acc) {
-  constexpr int EPV = Vec<DT>::EPV;
-  const int lane = threadIdx.x & 31;
-  const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
-  const bool direct = (k < Pr) || (c.N == 1);
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int c16 = lane + 32 * v;
-    if (c16 < c.cpr) {
-      const uint4 val = Vec<DT>::pack(acc + v * EPV);
-      if (direct) {
-        const int s = c16 / c.cps, cs = c16 - s * c.cps;
-        st16(recv_of(c, s, p, c.r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
-      } else {
-        st16(c.stage + ((size_t)p * c.max_tok + (k - Pr)) * row_bytes + (size_t)c16 * 16, val);
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -175,7 +154,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // into alpha_t, readings R3/R4): m += (1-b1)(g-m); v += (1-b2)(g^2-v);
 // w -= alpha_t m / (sqrt(v)+eps).  sqrt / reciprocal use the SFU (MUFU)
 // approximations: relative error ~1e-7, far inside the 1e-5 parity bound,
-// and an IEEE div+sqrt would be ~30 instructions per element.
+// where an IEEE div+sqrt would cost ~30 instructions per element.
 template <int EPV>
 __device__ __forceinline__ void opt_math(const DevCtx& c, float alpha, const float* g, float* w, float* mm, float* vv) {
   if (c.optim == SGD) {
@@ -193,24 +172,23 @@ __device__ __forceinline__ void opt_math(const DevCtx& c, float alpha, const flo
   }
 }
 
-// CTA-cooperative emission of coalesced rows parked in shared memory: row i
-// (D floats at rows + i*D) is slot ks[i] (skipped if < 0), shard row us[i].
+// CTA-cooperative emission of coalesced rows parked in shared memory: row j
+// (D floats at rows + j*D) is unique index ks[j] (skipped if < 0) of this
+// rank's source, id us[j], class pr[j] (1 = prior / single part).
 //   N == 1: the coalesced row IS the merged gradient of its id (one source):
-//           the optimizer step is applied here (no receive round trip, no
-//           merge kernel).  The row is first rounded to the wire dtype — the
-//           same rounding point as N > 1 (reading R11).
+//           the optimizer step is applied here.  The row is first rounded to
+//           the wire dtype — the same rounding point as N > 1 (reading R11).
 //   N > 1:  round to the wire dtype and store the column slices into the
-//           owners' receive rows (prior slots, NVLink) or the stage (scheduled).
-// Every thread handles EU (row, 16-byte chunk) items with all loads issued
-// before any use.
-template <int DT>
-__device__ __forceinline__ void emit_rows(const DevCtx& c, int p, int Pr, const float* rows, const int* ks,
-                                          const int* us, int nrows, float alpha) {
-  constexpr int EPV = Vec<DT>::EPV;
+//           owners' receive row i (prior rows, NVLink) or the stage (scheduled).
+// Every thread handles EU (row, 16-byte chunk) items, state loads first.
 #ifndef EMB_EU
 #define EMB_EU 8
 #endif
-  constexpr int EU = EMB_EU / EPV;  // (row, chunk) items in flight: 2 fp32 / 1 bf16
+template <int DT>
+__device__ __forceinline__ void emit_rows(const DevCtx& c, int p, const float* rows, const int* ks, const int* us,
+                                          const int* pr, int nrows, float alpha) {
+  constexpr int EPV = Vec<DT>::EPV;
+  constexpr int EU = EMB_EU / EPV;  // items in flight: 2 fp32 / 1 bf16
   const int total = nrows * c.cpr;
   const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
   const bool adam = (c.optim == ADAM);
@@ -274,11 +252,11 @@ __device__ __forceinline__ void emit_rows(const DevCtx& c, int p, int Pr, const 
 #pragma unroll
         for (int x = 0; x < EPV; ++x) g[x] = src[x];
         const uint4 val = Vec<DT>::pack(g);
-        if (k < Pr) {
+        if (pr[ii[j]]) {
           const int s = c16 / c.cps, cs = c16 - s * c.cps;
           st16(recv_of(c, s, p, c.r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
         } else {
-          st16(c.stage + ((size_t)p * c.max_tok + (k - Pr)) * row_bytes + (size_t)c16 * 16, val);
+          st16(c.stage + ((size_t)p * c.max_tok + k) * row_bytes + (size_t)c16 * 16, val);
         }
       }
     }
@@ -288,12 +266,12 @@ __device__ __forceinline__ void emit_rows(const DevCtx& c, int p, int Pr, const 
 // ------------------------------------------------------------------ sender coalesce
 // CTA b takes 8 consecutive chunks per round (one per warp).  Each warp
 // reduces its chunk (<= C rows, ascending position, fp32).  A single-chunk
-// slot's row is parked in shared memory and the CTA emits the parked rows
-// together (emit_rows).  Chunks of multi-chunk (Zipf-head) slots leave fp32
-// partials; the CTA then adds its chunk count to the slot's arrival counter,
-// and the CTA completing a slot combines all of its partials (warps sum
-// contiguous partial ranges, then a fixed-order shared-memory combine —
-// deterministic whichever CTA arrives last) and emits it.
+// unique's row is parked in shared memory and the CTA emits the parked rows
+// together.  Chunks of multi-chunk (Zipf-head) uniques leave fp32 partials;
+// the CTA then adds its chunk count to the unique's arrival counter, and the
+// CTA completing a unique combines all of its partials (warps sum contiguous
+// partial ranges, then a fixed-order shared-memory combine — deterministic
+// whichever CTA arrives last) and emits it.
 #ifndef EMB_COAL_MINB
 #define EMB_COAL_MINB 1  // 2 forces 128 registers and spills: measured 1.7x slower (round 1)
 #endif
@@ -303,23 +281,23 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float smem_f[];
   float* rows = smem_f;                        // [BWD_WARPS][D] parked single-chunk rows / combined row
-  float* comb = smem_f + BWD_WARPS * c.D;      // [BWD_WARPS][D] warp partials of a long slot
-  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS], s_ks[BWD_WARPS], s_us[BWD_WARPS];
+  float* comb = smem_f + BWD_WARPS * c.D;      // [BWD_WARPS][D] warp partials of a long unique
+  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS], s_ks[BWD_WARPS], s_us[BWD_WARPS],
+      s_pr[BWD_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
+  const uint32_t t = c.t_rec[p];
   const int* cnt = counts_of(c, p, r);
-  const int U = cnt[CNT_U], Pr = cnt[CNT_P], NCH = cnt[CNT_NCH];
+  const int U = cnt[CNT_U], NCH = cnt[CNT_NCH];
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int s = 0; s < c.N; ++s)
-      atomicAdd(&c.stats[c.N + s], (unsigned long long)(c.N == 1 ? U : Pr) * c.d * c.esz);
+    for (int s = 0; s < c.N; ++s) atomicAdd(&c.stats[c.N + s], (unsigned long long)U * c.d * c.esz);
   const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;
   const size_t bpn = pn(c, p, r) * (size_t)c.max_tok;
   const int* perm = c.perm + bpn;
-  const int* seg_start = c.seg_start + bpn;
-  const int* seg_end = c.seg_end + bpn;
-  const int* slot_id = c.slot_id + bpn;
+  const int* uid = c.uid + bpn;
+  const int* useg = c.useg + pn(c, p, r) * (size_t)(c.max_tok + 1);
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
-  const int* chunk_slot = c.chunk_slot + pn(c, p, r) * (size_t)c.max_chunks;
+  const int* chunk_uidx = c.chunk_uidx + pn(c, p, r) * (size_t)c.max_chunks;
   int* slot_ctr = c.slot_ctr + bpn;
   float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
   const size_t row_bytes = (size_t)c.D * c.esz;
@@ -329,24 +307,27 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
     {
       float acc[V * EPV];
       if (ch < NCH) {
-        k = chunk_slot[ch];
+        k = chunk_uidx[ch];
         const int c0 = chunk_off[k];
         nch = chunk_off[k + 1] - c0;
-        const int b = seg_start[k] + (ch - c0) * c.C;
-        const int e = min(seg_end[k], b + c.C);
+        const int b = useg[k] + (ch - c0) * c.C;
+        const int e = min(useg[k + 1], b + c.C);
         reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
         store_partial<EPV, V>((nch > 1) ? part + (size_t)ch * c.D : rows + (size_t)w * c.D, c.cpr, acc);
       }
     }
     if (lane == 0) {
+      const bool single = (ch < NCH && nch == 1);
       s_k[w] = (nch > 1) ? k : -1;
-      s_ks[w] = (ch < NCH && nch == 1) ? k : -1;
-      s_us[w] = (ch < NCH && nch == 1 && c.N == 1) ? slot_id[k] : 0;
+      s_ks[w] = single ? k : -1;
+      const int id = single ? uid[k] : 0;
+      s_us[w] = id;
+      s_pr[w] = single && (c.N == 1 || is_prior(c, p, t, id));
       s_last[w] = -1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      // distinct multi-chunk slots of this round (their chunks are consecutive)
+      // distinct multi-chunk uniques of this round (their chunks are consecutive)
       int nd = 0;
       for (int i = 0; i < BWD_WARPS; ++i) {
         if (s_k[i] < 0) continue;
@@ -367,7 +348,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
       __threadfence();
     }
     __syncthreads();
-    emit_rows<DT>(c, p, Pr, rows, s_ks, s_us, BWD_WARPS, alpha);
+    emit_rows<DT>(c, p, rows, s_ks, s_us, s_pr, BWD_WARPS, alpha);
     __syncthreads();
     for (int i = 0; i < BWD_WARPS; ++i) {
       const int kk = s_last[i];
@@ -387,11 +368,13 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
         rows[x] = sum;
       }
       if (threadIdx.x == 0) {
+        const int id = uid[kk];
         s_ks[0] = kk;
-        s_us[0] = (c.N == 1) ? slot_id[kk] : 0;
+        s_us[0] = id;
+        s_pr[0] = (c.N == 1 || is_prior(c, p, t, id));
       }
       __syncthreads();
-      emit_rows<DT>(c, p, Pr, rows, s_ks, s_us, 1, alpha);
+      emit_rows<DT>(c, p, rows, s_ks, s_us, s_pr, 1, alpha);
       __syncthreads();
     }
   }
@@ -402,18 +385,18 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
 __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
   pdl_wait();
   const int r = c.r;
-  const int* cnt = counts_of(c, p, r);
-  const int U = cnt[CNT_U], Pr = cnt[CNT_P], Q = U - Pr;
+  const uint32_t t = c.t_rec[p];
+  const int U = counts_of(c, p, r)[CNT_U];
+  const int* uid = c.uid + pn(c, p, r) * (size_t)c.max_tok;
   const size_t row_bytes = (size_t)c.D * c.esz, slice_bytes = (size_t)c.d * c.esz;
-  const size_t total = (size_t)Q * c.cpr;
+  const size_t total = (size_t)U * c.cpr;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-  if (tid == 0)
-    for (int s = 0; s < c.N; ++s) atomicAdd(&c.stats[c.N + s], (unsigned long long)Q * slice_bytes);
   for (size_t q = tid; q < total; q += nth) {
     const int k = (int)(q / c.cpr), c16 = (int)(q - (size_t)k * c.cpr);
+    if (is_prior(c, p, t, uid[k])) continue;  // prior rows went out with the coalesce
     const uint4 val = ld16_nc(c.stage + ((size_t)p * c.max_tok + k) * row_bytes + (size_t)c16 * 16);
     const int s = c16 / c.cps, cs = c16 - s * c.cps;
-    st16(recv_of(c, s, p, r) + (size_t)(Pr + k) * slice_bytes + (size_t)cs * 16, val);
+    st16(recv_of(c, s, p, r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
   }
   pdl_trigger();
 }
@@ -436,7 +419,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawpush_kernel(DevCtx c, const ch
   pdl_trigger();
 }
 
-// owner-side coalesce of every source's raw slices -> gc_owner (fp32)
+// owner-side coalesce of every source's raw slices -> gc_owner[n][i] (fp32)
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p) {
   pdl_wait();
@@ -463,10 +446,11 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
       if (n == m && ch >= nchs[m]) { ch -= nchs[m]; n = m + 1; }
     const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
     const int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
-    const int k = c.chunk_slot[pn(c, p, n) * (size_t)c.max_chunks + ch];
+    const int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
+    const int k = c.chunk_uidx[pn(c, p, n) * (size_t)c.max_chunks + ch];
     const int c0 = chunk_off[k], nch = chunk_off[k + 1] - c0;
-    const int b = c.seg_start[bpn + k] + (ch - c0) * c.C;
-    const int e = min(c.seg_end[bpn + k], b + c.C);
+    const int b = useg[k] + (ch - c0) * c.C;
+    const int e = min(useg[k + 1], b + c.C);
     reduce_rows<DT, V, true>(recv_of(c, c.r, p, n), slice_bytes, c.cps, c.perm + bpn, b, e, acc);
     float* dst = (nch > 1) ? c.scratch + (size_t)p * c.max_chunks * c.D + ((size_t)n * c.max_chunks + ch) * c.d
                            : c.gc_owner + (bpn + k) * (size_t)c.d;
@@ -495,7 +479,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p)
     for (int m = 0; m < EMB_WMAX - 1; ++m)
       if (n == m && li >= nls[m]) { li -= nls[m]; n = m + 1; }
     const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
-    const int k = c.long_slots[pn(c, p, n) * (size_t)c.max_long + li];
+    const int k = c.long_u[pn(c, p, n) * (size_t)c.max_long + li];
     const int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
     const int c0 = chunk_off[k], nch = chunk_off[k + 1] - c0;
     const int q0 = c0 + (int)((long long)nch * w / BWD_WARPS), q1 = c0 + (int)((long long)nch * (w + 1) / BWD_WARPS);
@@ -522,6 +506,10 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p)
 }
 
 // ------------------------------------------------------------------ owner merge + update
+// Items: every (source n, unique i) of the requested part (part 0: prior, or
+// everything outside SPLIT; part 1: scheduled).  The lowest source holding an
+// id (slotmap tag == t) applies it: contributions of all sources holding it
+// are summed in ascending source rank, then scaled and applied.
 template <int DT, bool RAWSRC>
 __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int part, int G) {
   pdl_wait();
@@ -534,36 +522,34 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
     if (threadIdx.x == 0) wait_all(c, flags_of(c, c.r)->pub[part], t);
     __syncthreads();
   }
-  int lo[EMB_WMAX], cnt[EMB_WMAX];
+  int cnt[EMB_WMAX];
   int total = 0;
 #pragma unroll
   for (int n = 0; n < EMB_WMAX; ++n) {
-    lo[n] = cnt[n] = 0;
-    if (n < c.N) {
-      const int* cn = counts_of(c, p, n);
-      const int U = cn[CNT_U], Pr = cn[CNT_P];
-      lo[n] = part ? Pr : 0;
-      cnt[n] = (part ? U : Pr) - lo[n];
-      total += cnt[n];
-    }
+    cnt[n] = (n < c.N) ? counts_of(c, p, n)[CNT_U] : 0;
+    total += cnt[n];
   }
-  const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;  // computed once by route(t)
-  const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
+  const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int grp = gtid / G, gl = gtid - grp * G, ngrp = (gridDim.x * blockDim.x) / G;
   const size_t slice_bytes = (size_t)c.d * c.esz;
   char* shard = shard_of(c, c.r);
+  const bool split = (c.mode == SPLIT);
   for (int item = grp; item < total; item += ngrp) {
     int n = 0, rem = item;
 #pragma unroll
     for (int m = 0; m < EMB_WMAX - 1; ++m)
       if (n == m && rem >= cnt[m]) { rem -= cnt[m]; n = m + 1; }
-    const int k = lo[n] + rem;
-    const int u = c.slot_id[pn(c, p, n) * (size_t)c.max_tok + k];
+    const int k = rem;
+    const int u = c.uid[pn(c, p, n) * (size_t)c.max_tok + k];
+    if (split) {
+      const bool pr = is_prior(c, p, t, u);
+      if (pr != (part == 0)) continue;  // the other part's row
+    }
     unsigned long long ent[EMB_WMAX];
     bool leader = true;
     if (c.N > 1) {
-      const unsigned long long* sm = c.slotmap + (size_t)u * c.N;
+      const unsigned long long* sm = c.slotmap + ((size_t)p * c.L + u) * c.N;
 #pragma unroll
       for (int n2 = 0; n2 < EMB_WMAX; ++n2) {
         ent[n2] = (n2 < c.N) ? sm[n2] : 0ull;
@@ -580,11 +566,9 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       char* wp = shard + (size_t)u * slice_bytes + (size_t)c16 * 16;
       const uint4 wraw = ld16(wp);
       float mm[EPV], vv[EPV];
-      float* mp = nullptr;
-      float* vp = nullptr;
+      float* mp = c.adam_m + (size_t)u * c.d + c16 * EPV;
+      float* vp = c.adam_v + (size_t)u * c.d + c16 * EPV;
       if (c.optim == ADAM) {
-        mp = c.adam_m + (size_t)u * c.d + c16 * EPV;
-        vp = c.adam_v + (size_t)u * c.d + c16 * EPV;
 #pragma unroll
         for (int i = 0; i < EPV; i += 4) {
           const float4 m4 = *reinterpret_cast<const float4*>(mp + i);
@@ -617,17 +601,8 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       }
       float w[EPV];
       Vec<DT>::unpack(wraw, w);
-      if (c.optim == SGD) {
-#pragma unroll
-        for (int i = 0; i < EPV; ++i) w[i] = w[i] - c.lr * (c.scale * g[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < EPV; ++i) {
-          const float gs = c.scale * g[i];
-          mm[i] = mm[i] + om_b1 * (gs - mm[i]);
-          vv[i] = vv[i] + om_b2 * (gs * gs - vv[i]);
-          w[i] = w[i] - alpha * mm[i] / (sqrtf(vv[i]) + c.eps);
-        }
+      opt_math<EPV>(c, alpha, g, w, mm, vv);
+      if (c.optim == ADAM) {
 #pragma unroll
         for (int i = 0; i < EPV; i += 4) {
           *reinterpret_cast<float4*>(mp + i) = make_float4(mm[i], mm[i + 1], mm[i + 2], mm[i + 3]);

@@ -32,6 +32,11 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
   const int nth = gridDim.x * blockDim.x;
   if (tid == 0) {
     c.t_rec[p] = t;
+    if (c.optim == ADAM) {
+      // Adam step size of iteration t, once (PyTorch SparseAdam form, readings R3/R4)
+      const double td = (double)t;
+      c.alpha[p] = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
+    }
     // the main stream has completed merge(prior, t-1) and (via the host's event
     // wait) merge(scheduled, t-2): publish them (see kernels.cuh protocol)
     if (t >= 2) publish(c, EMB_FLAG_OFF(prior_done), t - 1);

@@ -1,5 +1,5 @@
-// k_route.cu — per-source sort / unique (a6) and the Alg. 1 split + routing
-// tables (a5, a8) of SURVEY §8(a).
+// k_route.cu — per-source sort / unique / reduce chunks (a6), the prefetch
+// all-gather + D_next marks (a5) and the Alg. 1 slot tables (a8) of SURVEY §8(a).
 //
 // Alg. 1, lines 2-5:
 //   G_coalesced <- COALESCE(G)        — rows of equal id are summed (values: by
@@ -12,28 +12,29 @@
 // "The calculations require a considerable computing resource, and the GPU
 // idle time after BP is a good occasion".
 //
-// B200 design.  The expensive part — sorting every source's (id, position)
-// pairs — depends only on the gathered ids of iteration t, which the prefetch
-// makes available one iteration early.  So it is split off:
-//
-//   sort_kernel(t)   one CTA (1024 threads) per source, on an auxiliary stream,
-//                    launched as soon as ids(t) are gathered (normally right
-//                    after route(t-1)); it overlaps coal/merge of t-1 and the
-//                    forward of t.  LSD radix sort in shared memory over the
-//                    drop+id bits (stable => positions ascending inside a
-//                    segment); 4-bit digits ranked with thread-private u16
-//                    counters and one raking block scan per pass.  Output:
-//                    perm (positions in (dropped, id, pos) order), the ascending
-//                    unique kept ids uid[] and their segment starts useg[].
-//   route_kernel(t)  on the main stream in the backward ("after BP"): pushes
-//                    the next ids (prefetch all-gather), builds D_next as an
-//                    L-bit shared-memory bitmap, splits the unique ids into
-//                    prior / scheduled with a stable ballot partition (slot k:
-//                    prior ascending, then scheduled ascending), and emits the
-//                    slot tables, reduce chunks (C rows) and the multi-chunk
-//                    (Zipf-head) slot list.  Every rank does every source (the
-//                    owner merge needs all of them), so no size messages are
-//                    exchanged (reading R14).
+// B200 design:
+//   sort_kernel(t)   one CTA (1024 threads) per source on an auxiliary stream,
+//                    launched as soon as ids(t) are gathered — normally right
+//                    after mark(t-1), one iteration ahead — so it overlaps the
+//                    previous backward and the forward.  LSD radix sort in
+//                    shared memory over the drop+id bits (stable => positions
+//                    ascending inside a segment), 4-bit digits ranked with
+//                    thread-private u16 counters and one raking block scan per
+//                    pass.  Emits perm, the ascending unique kept ids uid[i],
+//                    their segments useg[i], the reduce chunks (C rows) per
+//                    unique, the multi-chunk (Zipf-head) list and, N > 1, the
+//                    owner routing slotmap[id][n] = (t, i).
+//   mark_kernel(t)   main stream: CTA n pushes this rank's next ids to peer n
+//                    (the prefetch all-gather) and, in SPLIT, marks D_next:
+//                    nextmark[p][id] = t+1 (epoch tag, never cleared).  The
+//                    split is then a per-id test in every backward kernel — no
+//                    prefix over the split on the critical path.
+//   tables_kernel(t) off the critical path: the Alg. 1 split in the paper's
+//                    presentation — slot k = prior ids ascending, then
+//                    scheduled ids ascending (P_n ++ D_n) and p_n — for the
+//                    statistics and the integer parity tests.
+//   Every rank sorts every source (the owner merge needs all of them; the
+//   gathered ids are local), so no size messages are exchanged (reading R14).
 #include <stddef.h>
 
 #include "kernels.cuh"
@@ -73,8 +74,8 @@ __device__ __forceinline__ int block_exscan(int v, int* tmp, int* total) {
   return before + x - v;
 }
 
-// Two-counter exclusive scan of per-warp totals held in wa[32], wb[32] by
-// warp 0; results back in place, grand totals in tot[0..1].
+// Two-counter exclusive scan of per-warp totals wa[32], wb[32] (warp 0 does
+// it); results back in place, grand totals in tot[0..1].
 __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {
   const int lane = threadIdx.x & 31;
   if ((threadIdx.x >> 5) == 0) {
@@ -97,7 +98,7 @@ template <typename K, int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, int fwd_pushed) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int kb = (c.max_tok + 1 + 3) & ~3;  // keys per buffer, 16-byte aligned
+  const int kb = (c.max_tok + 1 + 3) & ~3;  // keys per buffer (+1 for segs[U]), 16-byte aligned
   K* keyA = reinterpret_cast<K*>(smem_raw);
   K* keyB = keyA + kb;
   uint16_t* cnt = reinterpret_cast<uint16_t*>(keyB + kb);  // [NDIG][RT_THREADS]
@@ -108,8 +109,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   // t of the batch being sorted: this kernel runs either after forward(t) (ids
-  // pushed there) or after route(t-1) (prefetched) — before forward(t) wrote
-  // t_rec[p] — so derive it from the previous iteration's record.
+  // pushed there) or after mark(t-1) (prefetched) — possibly before forward(t)
+  // wrote t_rec[p] — so derive it from the previous iteration's record.
   const uint32_t tt = c.t_rec[p ^ 1] + 1;
   EMB_TS(20);
   if (n == 0 && tid == 0 && fwd_pushed) publish(c, EMB_FLAG_OFF(ids), tt);
@@ -135,10 +136,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
         int id = cur[k];
         int drop = 0;
         if ((unsigned)id >= (unsigned long long)L) {
-          id = (int)L;  // invalid: sentinel, dropped
+          id = (int)L;  // invalid: sentinel, dropped (the forward flags EMB_ERR_ID_RANGE)
           drop = 1;
         } else if (c.pad_id >= 0 && (long long)id == c.pad_id) {
-          drop = 1;
+          drop = 1;     // reading R6: pad rows get no gradient
         }
         keyA[i] = (K(drop) << dshift) | (K(id) << posbits) | K(i);
       }
@@ -200,17 +201,18 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   }
   EMB_TS(22);
 
-  // heads -> unique kept ids (ascending) + segment starts; perm = sorted positions
+  // ---- heads -> unique kept ids (ascending), segments, owner routing
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
   int* perm = c.perm + bpn;
   int* uid = c.uid + bpn;
   int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
+  int* segs = reinterpret_cast<int*>(keyB);  // shared copy of useg (keyB is free)
   const K posmask = (K(1) << posbits) - 1;
   const unsigned idmask = (1u << idbits) - 1u;
-  const int per_warp = (T + RT_WARPS - 1) / RT_WARPS;
-  const int w0 = min(T, w * per_warp), w1 = min(T, w0 + per_warp);
   int* wa = tmp;
   int* wb = tmp + 32;
+  const int per_warp = (T + RT_WARPS - 1) / RT_WARPS;
+  const int w0 = min(T, w * per_warp), w1 = min(T, w0 + per_warp);
   {
     int kept = 0;
     for (int base = w0; base < w1; base += 32) {
@@ -227,6 +229,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   int kbase = wa[w];
   const int U = s_tot[0];
   __syncthreads();
+  if (tid == 0) segs[U] = T;  // end of the last kept segment (a dropped head overwrites it)
+  __syncthreads();
   for (int base = w0; base < w1; base += 32) {
     const int i = base + lane;
     const bool valid = i < w1;
@@ -239,179 +243,31 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
       perm[i] = (int)(key & posmask);
       if (kept) {
         const int k = kbase + __popc(keptm & lt_mask);
-        uid[k] = (int)((key >> posbits) & idmask);
-        useg[k] = i;
+        const int id = (int)((key >> posbits) & idmask);
+        uid[k] = id;
+        segs[k] = i;
+        if (c.N > 1)
+          c.slotmap[((size_t)p * c.L + id) * c.N + n] = ((unsigned long long)tt << 32) | (unsigned)k;
       } else if (head && (i == 0 || (prev >> dshift) == 0)) {
-        useg[U] = i;  // first dropped element = end of the last kept segment
+        segs[U] = i;  // first dropped element = end of the last kept segment
       }
     }
     kbase += __popc(keptm);
   }
-  if (tid == 0) {
-    // end of the last kept segment when nothing is dropped (a dropped head wrote it otherwise)
-    int* cn = c.counts + pn(c, p, n) * CNT_W;
-    cn[CNT_ST] = T;
-    cn[CNT_SU] = U;
-  }
   __syncthreads();
-  if (tid == 0 && (T == 0 || (keyA[T - 1] >> dshift) == 0)) useg[U] = T;
   EMB_TS(23);
-  pdl_trigger();
-}
 
-// ============================================================== route (main stream)
-template <int EPT>
-__global__ void __launch_bounds__(RT_THREADS, 1) route_kernel(DevCtx c, int p, const int* __restrict__ next_ids,
-                                                              int n_next) {
-  pdl_wait();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem_raw);  // D_next, ceil(L/32) words
-  __shared__ int s_tmp[64];
-  __shared__ int s_tot[2];
-
-  const int n = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const uint32_t t = c.t_rec[p];
-  const int p1 = p ^ 1;
-  const bool split = (c.mode == SPLIT);
-  const bool has_next = (next_ids != nullptr);
-  const long long L = c.L;
-  EMB_TS(0);
-  if (n == 0 && tid == 0 && c.optim == ADAM) {
-    // Adam step size of this iteration, once (PyTorch SparseAdam form, reading R3/R4)
-    const double td = (double)t;
-    c.alpha[p] = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
-  }
-
-  // ---- 1. prefetch all-gather: CTA n pushes this rank's next ids to peer n
-  if (has_next) {
-    int* dst = gids_of(c, n, p1, c.r);
-    int v[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int j = tid + k * RT_THREADS;
-      if (j < n_next) v[k] = __ldg(next_ids + j);
-    }
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int j = tid + k * RT_THREADS;
-      if (j < n_next) dst[j] = v[k];
-    }
-    if (tid == 0) {
-      *ntok_of(c, n, p1, c.r) = n_next;
-      atomicAdd(&c.stats[2 * c.N + n], (unsigned long long)n_next * 4ull);
-    }
-    __syncthreads();
-    if (tid == 0 && c.N > 1) {
-      __threadfence_system();
-      st_release_sys(&flags_of(c, n)->ids[c.r], t + 1);
-    }
-  }
-
-  // ---- 2. unique ids of source n (from sort(t)) into registers
-  const int* cn = counts_of(c, p, n);
-  const int U = cn[CNT_SU];
-  const int Tn = cn[CNT_ST];
-  const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
-  const int* uid = c.uid + bpn;
-  const int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
-  // warp-contiguous ranges of unique ids, lane-striped rounds
+  // ---- reduce chunks (C rows) per unique, chunk -> unique, multi-chunk list
+  int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
+  int* chunk_uidx = c.chunk_uidx + pn(c, p, n) * (size_t)c.max_chunks;
+  int* long_u = c.long_u + pn(c, p, n) * (size_t)c.max_long;
   const int per_w = (U + RT_WARPS - 1) / RT_WARPS;
   const int k0w = min(U, w * per_w), k1w = min(U, k0w + per_w);
-  constexpr int RMAX = (EPT * RT_THREADS / RT_WARPS + 31) / 32;  // rounds per warp (U <= max_tok)
-  int uv[RMAX], sa[RMAX], sb[RMAX];
-#pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    const int k = k0w + r * 32 + lane;
-    uv[r] = (k < k1w) ? uid[k] : -1;
-    sa[r] = (k < k1w) ? useg[k] : 0;
-    sb[r] = (k < k1w) ? useg[k + 1] : 0;
-  }
-  EMB_TS(1);
-
-  // ---- 3. D_next bitmap (gathered next batch of every rank)
-  if (split && has_next) {
-    const int nwords = (int)((L + 31) >> 5);
-    for (int i = tid; i < nwords; i += RT_THREADS) bitmap[i] = 0u;
-    if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1);
-    __syncthreads();
-    for (int s = 0; s < c.N; ++s) {
-      const int cnx = __ldcg(ntok_of(c, c.r, p1, s));
-      const int* gn = gids_of(c, c.r, p1, s);
-      int v[EPT];
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const int j = tid + k * RT_THREADS;
-        v[k] = (j < cnx) ? __ldcg(gn + j) : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < EPT; ++k)
-        if ((unsigned)v[k] < (unsigned long long)L) atomicOr(&bitmap[v[k] >> 5], 1u << (v[k] & 31));
-    }
-    __syncthreads();
-  }
-  EMB_TS(2);
-
-  // ---- 4. stable partition of the unique ids: prior (in D_next) first
-  auto is_prior = [&](int id) {
-    return !split || (has_next && ((bitmap[id >> 5] >> (id & 31)) & 1u));
-  };
-  int* wa = s_tmp;
-  int* wb = s_tmp + 32;
-  {
-    int pri = 0, nch_sum = 0;
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      const bool valid = uv[r] >= 0;
-      pri += __popc(__ballot_sync(0xffffffffu, valid && is_prior(uv[r])));
-    }
-    if (lane == 0) { wa[w] = pri; wb[w] = nch_sum; }
-    __syncthreads();
-    warp_totals_scan(wa, wb, s_tot);
-  }
-  const int P_tot = s_tot[0];
-  int pbase = wa[w];                 // prior heads before this warp
-  int dbase = k0w - wa[w];           // scheduled heads before this warp (k0w = all heads before)
-  __syncthreads();
-  int* slot_id = c.slot_id + bpn;
-  int* seg_start = c.seg_start + bpn;
-  int* seg_end = c.seg_end + bpn;
-  int kslot[RMAX];
-#pragma unroll
-  for (int r = 0; r < RMAX; ++r) {
-    const bool valid = uv[r] >= 0;
-    const bool pr = valid && is_prior(uv[r]);
-    const unsigned pm = __ballot_sync(0xffffffffu, pr);
-    const unsigned dm = __ballot_sync(0xffffffffu, valid && !pr);
-    kslot[r] = -1;
-    if (valid) {
-      const int k = pr ? pbase + __popc(pm & lt_mask) : P_tot + dbase + __popc(dm & lt_mask);
-      kslot[r] = k;
-      slot_id[k] = uv[r];
-      seg_start[k] = sa[r];
-      seg_end[k] = sb[r];
-      if (c.N > 1) c.slotmap[(size_t)uv[r] * c.N + n] = ((unsigned long long)t << 32) | (unsigned)k;
-    }
-    pbase += __popc(pm);
-    dbase += __popc(dm);
-  }
-  __syncthreads();  // slot tables complete (block scope)
-  EMB_TS(3);
-
-  // ---- 5. reduce chunks in slot order (C rows each) and the long-slot list
-  int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
-  int* chunk_slot = c.chunk_slot + pn(c, p, n) * (size_t)c.max_chunks;
-  int* long_slots = c.long_slots + pn(c, p, n) * (size_t)c.max_long;
-  int nch[RMAX], kk[RMAX];
   {
     int wch = 0, wlg = 0;
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      const int k = k0w + r * 32 + lane;  // slot-ordered walk (global memory, block-visible)
-      kk[r] = k;
-      int x = (k < k1w) ? (seg_end[k] - seg_start[k] + c.C - 1) / c.C : 0;
-      nch[r] = x;
+    for (int base = k0w; base < k1w; base += 32) {
+      const int k = base + lane;
+      int x = (k < k1w) ? (segs[k + 1] - segs[k] + c.C - 1) / c.C : 0;
       wlg += __popc(__ballot_sync(0xffffffffu, x > 1));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -424,38 +280,132 @@ __global__ void __launch_bounds__(RT_THREADS, 1) route_kernel(DevCtx c, int p, c
   const int NCH = s_tot[0], NLONG = s_tot[1];
   {
     int cb = wa[w], lb = wb[w];
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      const int k = kk[r];
+    for (int base = k0w; base < k1w; base += 32) {
+      const int k = base + lane;
       const bool valid = k < k1w;
-      int incl = nch[r];
+      const int a = valid ? segs[k] : 0, b = valid ? segs[k + 1] : 0;
+      const int nch = valid ? (b - a + c.C - 1) / c.C : 0;
+      int incl = nch;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      const unsigned longm = __ballot_sync(0xffffffffu, nch[r] > 1);
+      const unsigned longm = __ballot_sync(0xffffffffu, nch > 1);
       if (valid) {
-        const int off = cb + incl - nch[r];
+        const int off = cb + incl - nch;
+        useg[k] = a;
         chunk_off[k] = off;
-        for (int q = 0; q < nch[r]; ++q) chunk_slot[off + q] = k;
-        if (nch[r] > 1) long_slots[lb + __popc(longm & lt_mask)] = k;
+        for (int q = 0; q < nch; ++q) chunk_uidx[off + q] = k;
+        if (nch > 1) long_u[lb + __popc(longm & lt_mask)] = k;
       }
       cb += __shfl_sync(0xffffffffu, incl, 31);
       lb += __popc(longm);
     }
   }
   if (tid == 0) {
+    useg[U] = segs[U];
     chunk_off[U] = NCH;
-    int* cw = c.counts + pn(c, p, n) * CNT_W;
-    cw[CNT_T] = Tn;
-    cw[CNT_U] = U;
-    cw[CNT_P] = P_tot;
-    cw[CNT_NCH] = NCH;
-    cw[CNT_NLONG] = NLONG;
+    int* cn = c.counts + pn(c, p, n) * CNT_W;
+    cn[CNT_T] = T;
+    cn[CNT_U] = U;
+    cn[CNT_NCH] = NCH;
+    cn[CNT_NLONG] = NLONG;
   }
-  (void)kslot;
-  EMB_TS(4);
+  EMB_TS(24);
+  pdl_trigger();
+}
+
+// ============================================================== mark (main stream)
+// CTA s pushes this rank's next ids to peer s (prefetch all-gather; the flag is
+// released by that CTA after its own stores), then with do_mark (SPLIT) all
+// CTAs wait for every rank's next ids and tag D_next: nextmark[p][id] = t+1.
+__global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* __restrict__ next_ids, int n_next,
+                                                    int do_mark) {
+  pdl_wait();
+  const uint32_t t = c.t_rec[p];
+  const int p1 = p ^ 1;
+  const int tid = threadIdx.x;
+  if (next_ids != nullptr) {
+    for (int s = blockIdx.x; s < c.N; s += gridDim.x) {
+      int* dst = gids_of(c, s, p1, c.r);
+      for (int j = tid; j < n_next; j += blockDim.x) dst[j] = __ldg(next_ids + j);
+      if (tid == 0) {
+        *ntok_of(c, s, p1, c.r) = n_next;
+        atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n_next * 4ull);
+      }
+      __syncthreads();
+      if (tid == 0 && c.N > 1) {
+        __threadfence_system();
+        st_release_sys(&flags_of(c, s)->ids[c.r], t + 1);
+      }
+    }
+  }
+  if (do_mark && next_ids != nullptr) {
+    if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1);  // grid = N CTAs: co-resident
+    __syncthreads();
+    int* mark = c.nextmark + (size_t)p * c.L;
+    const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
+    for (int s = 0; s < c.N; ++s) {
+      const int cn = __ldcg(ntok_of(c, c.r, p1, s));
+      const int* gn = gids_of(c, c.r, p1, s);
+      for (int j = gtid; j < cn; j += nthr) {
+        const int id = __ldcg(gn + j);
+        if ((unsigned)id < (unsigned long long)c.L) mark[id] = (int)(t + 1);
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+// ============================================================== Alg. 1 tables (off the critical path)
+// Slot order of the paper's presentation: P_n = U_n ∩ D_next ascending, then
+// D_n = U_n \ P_n ascending (a stable ballot partition of the unique ids).
+template <int EPT>
+__global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) {
+  pdl_wait();
+  __shared__ int s_tmp[64];
+  __shared__ int s_tot[2];
+  const int n = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t t = c.t_rec[p];
+  const int U = counts_of(c, p, n)[CNT_U];
+  const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
+  const int* uid = c.uid + bpn;
+  int* slot_id = c.slot_id + bpn;
+  const int per_w = (U + RT_WARPS - 1) / RT_WARPS;
+  const int k0w = min(U, w * per_w), k1w = min(U, k0w + per_w);
+  constexpr int RMAX = EPT;  // rounds per warp: U <= max_tok <= EPT * 1024
+  int uv[RMAX];
+  bool pr[RMAX];
+  int pri = 0;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    const int k = k0w + r * 32 + lane;
+    uv[r] = (k < k1w) ? uid[k] : -1;
+  }
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    pr[r] = uv[r] >= 0 && is_prior(c, p, t, uv[r]);
+    pri += __popc(__ballot_sync(0xffffffffu, pr[r]));
+  }
+  if (lane == 0) { s_tmp[w] = pri; s_tmp[32 + w] = 0; }
+  __syncthreads();
+  warp_totals_scan(s_tmp, s_tmp + 32, s_tot);
+  const int P_tot = s_tot[0];
+  int pbase = s_tmp[w];
+  int dbase = k0w - s_tmp[w];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    const bool valid = uv[r] >= 0;
+    const unsigned pm = __ballot_sync(0xffffffffu, pr[r]);
+    const unsigned dm = __ballot_sync(0xffffffffu, valid && !pr[r]);
+    if (valid) slot_id[pr[r] ? pbase + __popc(pm & lt_mask) : P_tot + dbase + __popc(dm & lt_mask)] = uv[r];
+    pbase += __popc(pm);
+    dbase += __popc(dm);
+  }
+  if (tid == 0) c.counts[pn(c, p, n) * CNT_W + CNT_P] = P_tot;
   pdl_trigger();
 }
 
@@ -472,8 +422,6 @@ size_t sort_smem_bytes(int max_tok, bool key64) {
   return (size_t)2 * ((max_tok + 1 + 3) & ~3) * (key64 ? 8 : 4) + (size_t)NDIG * RT_THREADS * 2 + 64 * 4;
 }
 
-size_t route_smem_bytes(long long vocab) { return (size_t)((vocab + 31) / 32) * 4 + 16; }
-
 template <typename K>
 static void* sort_fn(int ept) {
   switch (ept) {
@@ -488,27 +436,23 @@ static void* sort_fn(int ept) {
   return nullptr;
 }
 
-static void* route_fn(int ept) {
+static void* tables_fn(int ept) {
   switch (ept) {
-    case 1: return (void*)route_kernel<1>;
-    case 2: return (void*)route_kernel<2>;
-    case 4: return (void*)route_kernel<4>;
-    case 5: return (void*)route_kernel<5>;
-    case 8: return (void*)route_kernel<8>;
-    case 12: return (void*)route_kernel<12>;
-    case 16: return (void*)route_kernel<16>;
+    case 1: return (void*)tables_kernel<1>;
+    case 2: return (void*)tables_kernel<2>;
+    case 4: return (void*)tables_kernel<4>;
+    case 5: return (void*)tables_kernel<5>;
+    case 8: return (void*)tables_kernel<8>;
+    case 12: return (void*)tables_kernel<12>;
+    case 16: return (void*)tables_kernel<16>;
   }
   return nullptr;
 }
 
-cudaError_t route_set_smem(int max_tok, bool key64, size_t sort_smem, size_t route_smem) {
-  const int e = ept_for(max_tok);
-  void* f = key64 ? sort_fn<unsigned long long>(e) : sort_fn<uint32_t>(e);
-  void* g = route_fn(e);
-  if (!f || !g) return cudaErrorInvalidValue;
-  cudaError_t st = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem);
-  if (st != cudaSuccess) return st;
-  return cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_smem);
+cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem) {
+  void* f = key64 ? sort_fn<unsigned long long>(ept_for(max_tok)) : sort_fn<uint32_t>(ept_for(max_tok));
+  if (!f) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size_t smem, cudaStream_t s) {
@@ -519,12 +463,18 @@ cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size
   return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), smem, s, args);
 }
 
-cudaError_t launch_route(const DevCtx& c, int p, const int* next_ids, int n_next, size_t smem, cudaStream_t s) {
-  void* f = route_fn(ept_for(c.max_tok));
+cudaError_t launch_mark(const DevCtx& c, const LaunchCfg& L, int p, const int* next_ids, int n_next, int do_mark,
+                        cudaStream_t s) {
+  (void)L;
+  return launch_pdl(mark_kernel, dim3(c.N), dim3(1024), 0, s, c, p, next_ids, n_next, do_mark);
+}
+
+cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
+  void* f = tables_fn(ept_for(c.max_tok));
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
-  void* args[] = {&cc, &p, &next_ids, &n_next};
-  return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), smem, s, args);
+  void* args[] = {&cc, &p};
+  return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), 0, s, args);
 }
 
 }  // namespace emb

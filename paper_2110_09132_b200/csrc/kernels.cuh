@@ -44,22 +44,31 @@ inline cudaError_t launch_pdl_raw(const void* f, dim3 grid, dim3 block, size_t s
 // after it by an event), which starts only after the producer completed,
 // publishes the producer's flag to every peer (one thread, one system fence),
 // then waits for the peers' flags.  N == 1 skips the protocol (stream order).
+//
+// Rows of the backward are addressed by the sender's UNIQUE index i (the
+// ascending unique ids of the sort), not by Alg. 1 slot: the split into prior /
+// scheduled is an epoch-tagged mark of D_next that every kernel tests per id,
+// so no prefix over the split sits on the critical path.  The slot-ordered
+// Alg. 1 tables (P_n, D_n) are produced off the critical path (tables).
 
-// a1-a4: forward (publish prior_done/def_done of earlier iterations, id push or
-// prefetch check, wait for every owner, pull-gather)
+// a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
+// id push or prefetch check, wait for every owner, pull-gather)
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
                        int prefetched, cudaStream_t s);
-// a6: per-source sort by (dropped, id, position) + unique ids (auxiliary stream)
+// a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
+// owner routing (slotmap) — auxiliary stream, one iteration ahead
 cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size_t smem, cudaStream_t s);
-// a5 + a8: prefetch all-gather of the next ids, D_next bitmap, Alg. 1 split of
-// every source's unique ids into prior / scheduled slots, reduce chunks
-cudaError_t launch_route(const DevCtx& c, int p, const int* next_ids, int n_next, size_t smem, cudaStream_t s);
 size_t sort_smem_bytes(int max_tok, bool key64);
-size_t route_smem_bytes(long long vocab);
-cudaError_t route_set_smem(int max_tok, bool key64, size_t sort_smem, size_t route_smem);
-// a7 + a9 (+a10 for the prior part): sender coalesce.  coal_a: one warp per
-// chunk of <= C rows (single-chunk slots emitted directly, others leave fp32
-// partials); coal_b: one CTA per multi-chunk slot, fixed-order combine.
+cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
+// a5: prefetch all-gather of the next ids + D_next epoch marks (Alg. 1 line 4's set)
+cudaError_t launch_mark(const DevCtx& c, const LaunchCfg& L, int p, const int* next_ids, int n_next, int do_mark,
+                        cudaStream_t s);
+// a8 presentation: Alg. 1 slot tables P_n ++ D_n, counts p_n (stats / debug; off the critical path)
+cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s);
+// a7 + a9 (+a10 for the prior part): sender coalesce — segmented reduce in
+// fp32, long (Zipf-head) segments combined by the last-arriving CTA; N == 1
+// applies the optimizer directly, N > 1 pushes prior rows to the owners and
+// stages scheduled rows.
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s);
 // a12: push the staged scheduled rows to their owners (N > 1)
 cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);

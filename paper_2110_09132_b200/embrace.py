@@ -61,8 +61,8 @@ class EmbStats(ctypes.Structure):
                 ("err_flags", ctypes.c_int32), ("kernel_launches", ctypes.c_int64)]
 
 
-KERNEL_NAMES = ["fwd_pull_gather", "sort_unique", "route_split", "coal_push", "merge_update_prior",
-                "defpush", "merge_update_sched", "rawpush", "rawcoal"]
+KERNEL_NAMES = ["fwd_pull_gather", "sort_unique", "mark_next", "coal_push", "merge_update_prior",
+                "defpush", "merge_update_sched", "rawpush", "rawcoal", "split_tables"]
 EMB_NUM_KERNELS = len(KERNEL_NAMES)
 
 
