@@ -300,10 +300,16 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    def check_err(phase):  # sticky device error bits (1 id range, 2 state, 4 peer-wait timeout)
+        torch.cuda.synchronize()
+        ef = ex.stats()["err_flags"]
+        if ef:
+            raise RuntimeError(f"rank {rank}: device error flags {ef} after the {phase}")
+
     for k in range(args.warmup):
         step(k)
     E.emb_join(ex.ctx, stream)
-    torch.cuda.synchronize()
+    check_err("warm-up")
 
     # CUDA graph of one full cycle of nb steps (device-resident iteration counter -> replay-safe)
     graph = None
@@ -345,6 +351,9 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = ev0.elapsed_time(ev1)
+    check_err("timed region")
+    if os.environ.get("EMB_TRACE_OUT"):  # kernel trace ring (EMB_TRACE builds; scripts/trace.py)
+        np.save(f"{os.environ['EMB_TRACE_OUT']}.{rank}.npy", E.emb_debug_copy(ex.ctx, E.EMB_DBG_TIMESTAMPS))
     kk = k0 + rem                  # next batch index (graph replays are whole cycles)
     t_max = ms
     if world > 1:
@@ -363,6 +372,7 @@ def main():
     E.emb_join(ex.ctx, stream)
     prof = E.emb_profile_read(ex.ctx)
     E.emb_profile(ex.ctx, False)
+    check_err("profile")
     # kernels per step: count the profiled launches (one step = one fwd + one bwd)
     per_step_launch = sum(c for (_, c) in prof.values()) / P
     k_prof = kk

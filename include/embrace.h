@@ -120,7 +120,8 @@ typedef enum {
   EMB_K_RAWPUSH = 7,  /* RAW a10 raw slice push                                   */
   EMB_K_RAWCOAL = 8,  /* RAW owner-side coalesce                                  */
   EMB_K_TABLES = 9,   /* a8 Alg. 1 slot tables P_n ++ D_n (off the critical path) */
-  EMB_NUM_KERNELS = 10
+  EMB_K_GATE = 10,    /* N > 1 peer-flag gate (one warp: publish + wait)           */
+  EMB_NUM_KERNELS = 11
 } emb_kernel_kind;
 
 /* Debug items for emb_debug_copy (integer parity tests). `src` selects the
@@ -133,7 +134,8 @@ typedef enum {
   EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src sorted by (dropped, id,
                            position); slot k's rows are perm[seg_start[k] .. seg_end[k]) */
   EMB_DBG_ISSUE_LOG = 4, /* int64 [k]     dense-queue tickets in issue order          */
-  EMB_DBG_TIMESTAMPS = 5  /* uint64 [64]   device phase timestamps (EMB_PHASE_TIMING builds) */
+  EMB_DBG_TIMESTAMPS = 5  /* uint64 [16][16][4] kernel trace ring: [t%16][kernel kind][entered,
+                             waited, finished] globaltimer ns (EMB_TRACE builds; zeros otherwise) */
 } emb_debug_item;
 
 typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1, EMB_STATE_ADAM_V = 2 } emb_state_item;

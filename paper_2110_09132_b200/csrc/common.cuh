@@ -83,19 +83,38 @@ struct DevCtx {
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
-  unsigned long long* dbg_ts; // [64] phase timestamps (EMB_PHASE_TIMING builds only)
+  unsigned long long* dbg_ts; // [EMB_TRACE_SLOTS] kernel trace (EMB_TRACE builds only)
 };
 
-#ifdef EMB_PHASE_TIMING
-#define EMB_TS(i)                                                       \
-  do {                                                                  \
-    if (threadIdx.x == 0 && blockIdx.x == 0) c.dbg_ts[i] = globaltimer(); \
+// Kernel trace (EMB_TRACE builds only; a debug aid, compiled out otherwise):
+// dbg_ts[(t & 15)][kind][8] globaltimer stamps — 0: block 0 entered (before
+// the PDL wait), 1: block 0 past its dependency/flag waits, 2: last block
+// finished (max over blocks), 3..7: block 0 at kernel-specific points
+// (EMB_TR_AT).  Read with emb_debug_copy(EMB_DBG_TIMESTAMPS).
+#define EMB_TRACE_SLOTS (16 * 16 * 8)
+#ifdef EMB_TRACE
+#define EMB_TR_IDX(kind, t, slot) (((((t)&15) * 16) + (kind)) * 8 + (slot))
+#define EMB_TR_ENTRY() const unsigned long long tr_entry_ = globaltimer()
+#define EMB_TR_BEGIN(kind, t)                                                             \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.dbg_ts[EMB_TR_IDX(kind, t, 0)] = tr_entry_; \
+  } while (0)
+#define EMB_TR_AT(kind, t, slot)                                                              \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.dbg_ts[EMB_TR_IDX(kind, t, slot)] = globaltimer(); \
+  } while (0)
+#define EMB_TR_END(kind, t)                                                              \
+  do {                                                                                   \
+    if (threadIdx.x == 0) atomicMax(c.dbg_ts + EMB_TR_IDX(kind, t, 2), globaltimer());   \
   } while (0)
 #else
-#define EMB_TS(i) \
-  do {            \
-  } while (0)
+#define EMB_TR_ENTRY() do {} while (0)
+#define EMB_TR_BEGIN(kind, t) do {} while (0)
+#define EMB_TR_AT(kind, t, slot) do {} while (0)
+#define EMB_TR_END(kind, t) do {} while (0)
 #endif
+#define EMB_TR_WAITED(kind, t) EMB_TR_AT(kind, t, 1)
+#define EMB_TR_MID(kind, t) EMB_TR_AT(kind, t, 3)
 
 // ----------------------------------------------------------------- addressing
 __device__ __forceinline__ char* shard_of(const DevCtx& c, int s) { return c.sym[s] + c.lay.shard; }
@@ -129,6 +148,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Message-passing release at system scope: acq_rel (not sc) is what the
+// data -> flag pattern needs; it is cumulative over what this thread observed
+// (the completed producer grid after griddepcontrol.wait, or its CTA's stores
+// after __syncthreads).
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -156,17 +183,28 @@ __device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags,
 }
 
 // Publish value v into slot [c.r] of field `field` (an offset into Flags) of
-// every rank's flags.  Called by ONE thread at the start of the kernel that
-// follows the producer on the same stream: the producer has completed, so its
-// stores (local and peer) are performed; the system fence + release store make
-// them visible to the peer before the flag.
-__device__ __forceinline__ void publish(const DevCtx& c, size_t field_off, uint32_t v) {
-  if (c.N == 1) return;
-  __threadfence_system();
+// every rank's flags.  Called by ONE thread of the kernel that follows the
+// producer, after griddepcontrol.wait (same stream) or a full graph/event
+// dependency (other stream): the producer grid has COMPLETED, and grid
+// completion includes the end-of-grid system-scope memory flush (the one that
+// makes a finished kernel's stores — local, peer and host-mapped — visible to
+// the host after an event).  Every producer store is therefore performed at
+// system scope before this thread runs, and the flag needs no fence of its
+// own: a relaxed system-scope store suffices.
+// A fence.sys here cost 2-7 us per publish on B200 under concurrent NVLink
+// traffic (kernel trace, profiles/r01_trace_n2.txt).  Stores made by the SAME
+// kernel before a flag (mark) still take fence_acq_rel_sys().
+__device__ __forceinline__ void publish2(const DevCtx& c, size_t off_a, uint32_t va, bool do_a, size_t off_b,
+                                         uint32_t vb, bool do_b) {
+  if (c.N == 1 || !(do_a || do_b)) return;
   for (int s = 0; s < c.N; ++s) {
-    uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(flags_of(c, s)) + field_off) + c.r;
-    st_release_sys(f, v);
+    char* f = reinterpret_cast<char*>(flags_of(c, s));
+    if (do_a) st_relaxed_sys(reinterpret_cast<uint32_t*>(f + off_a) + c.r, va);
+    if (do_b) st_relaxed_sys(reinterpret_cast<uint32_t*>(f + off_b) + c.r, vb);
   }
+}
+__device__ __forceinline__ void publish(const DevCtx& c, size_t field_off, uint32_t v) {
+  publish2(c, field_off, v, true, 0, 0, false);
 }
 #define EMB_FLAG_OFF(member) offsetof(::emb::Flags, member)
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -140,6 +141,12 @@ static cudaError_t run_k(emb_ctx* ctx, int kind, cudaStream_t s, F&& fn) {
   return e;
 }
 
+// N > 1 peer-flag gate before a consumer kernel (k_gate.cu); nothing at N == 1
+static cudaError_t gate(emb_ctx* ctx, int p, int kind, int flag_arg, cudaStream_t s) {
+  if (ctx->pl.N == 1) return cudaSuccess;
+  return run_k(ctx, EMB_K_GATE, s, [&] { return launch_gate(ctx->dc, p, kind, flag_arg, s); });
+}
+
 #define CKC(ctx, call)                                                                   \
   do {                                                                                  \
     cudaError_t e_ = (call);                                                            \
@@ -253,7 +260,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
     ALLOC(c.stats, 3 * N * 8);
-    ALLOC(c.dbg_ts, 64 * 8);
+    ALLOC(c.dbg_ts, EMB_TRACE_SLOTS * 8);
   }
 #undef ALLOC
   if (sort_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem) != cudaSuccess) goto fail;
@@ -366,12 +373,14 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     ctx->mark_pending = false;
   }
   const int pre = ctx->prefetched ? 1 : 0;
+  CKC(ctx, gate(ctx, p, GATE_FWD, 0, stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
     CKC(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_main[p], 0));
+    CKC(ctx, gate(ctx, p, GATE_SORT, 1, ctx->aux));
     CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux, [&] {
       return launch_sort(ctx->dc, p, 1, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
     }));
@@ -425,6 +434,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // a6 for the next batch, one iteration ahead.  Its parity's previous user
     // (the scheduled merge of t-1) must be done with the routing tables.
     if (ctx->def_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_def[p ^ 1], 0));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 0, aux));
     CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] { return launch_sort(c, p ^ 1, 0, ctx->pl.key64, ctx->pl.sort_smem, aux); }));
     CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
     ctx->sort_pending[p ^ 1] = true;
@@ -435,20 +445,24 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   }
   if (mode == EMB_BWD_RAW) {
     CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
+    CKC(ctx, gate(ctx, p, GATE_PUB0, 0, stream));
     CKC(ctx, run_k(ctx, EMB_K_RAWCOAL, stream, [&] { return launch_rawcoal(c, lc, p, stream); }));
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.
-    if (ctx->pl.N > 1)
+    if (ctx->pl.N > 1) {
+      CKC(ctx, gate(ctx, p, GATE_PUB0, 0, stream));
       CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
+    }
     if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) {
       // scheduled part: lowest-priority side stream, after the prior part
       CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));
       CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));
       if (ctx->pl.N > 1)  // N == 1: coal wrote every row to its receive slot directly
         CKC(ctx, run_k(ctx, EMB_K_DEFPUSH, side, [&] { return launch_defpush(c, lc, p, side); }));
+      CKC(ctx, gate(ctx, p, GATE_PUB1, 0, side));
       CKC(ctx, run_k(ctx, EMB_K_MERGE1, side, [&] { return launch_merge(c, lc, p, 1, side); }));
       CKC(ctx, cudaEventRecord(ctx->ev_def[p], ctx->side));
       ctx->def_pending[p] = true;
@@ -551,15 +565,31 @@ emb_status emb_profile_read(emb_ctx* ctx, double* ms, int64_t* count) {
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
   CKC(ctx, cudaDeviceSynchronize());
   for (int k = 0; k < EMB_NUM_KERNELS; ++k) { ms[k] = 0.0; count[k] = 0; }
+  // EMB_PROF_TIMELINE=<file>: append "kind start_us dur_us" per launch (debug aid)
+  FILE* tl = nullptr;
+  if (const char* tp = getenv("EMB_PROF_TIMELINE")) {
+    char path[512];
+    snprintf(path, sizeof path, "%s.%d", tp, ctx->cfg.rank);
+    tl = fopen(path, "a");
+  }
   for (auto& r : ctx->prof_recs) {
     float t = 0.f;
+    if (tl) {
+      float t0 = 0.f, d = 0.f;
+      cudaEventElapsedTime(&t0, ctx->prof_recs.front().a, r.a);
+      cudaEventElapsedTime(&d, r.a, r.b);
+      fprintf(tl, "%d %.2f %.2f\n", r.kind, t0 * 1e3f, d * 1e3f);
+    }
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
       ms[r.kind] += t;
       count[r.kind] += 1;
     }
+  }
+  for (auto& r : ctx->prof_recs) {  // after the loop: the timeline measures from the first event
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
+  if (tl) fclose(tl);
   ctx->prof_recs.clear();
   return EMB_OK;
 }
@@ -606,9 +636,9 @@ emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, s
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
   CKC(ctx, cudaDeviceSynchronize());
   if (item == EMB_DBG_TIMESTAMPS) {
-    *n = 64;
-    if (cap < 64 * 8) return EMB_ERR_CAPACITY;
-    CKC(ctx, cudaMemcpy(host, ctx->dc.dbg_ts, 64 * 8, cudaMemcpyDeviceToHost));
+    *n = EMB_TRACE_SLOTS;
+    if (cap < EMB_TRACE_SLOTS * 8) return EMB_ERR_CAPACITY;
+    CKC(ctx, cudaMemcpy(host, ctx->dc.dbg_ts, EMB_TRACE_SLOTS * 8, cudaMemcpyDeviceToHost));
     return EMB_OK;
   }
   if (item == EMB_DBG_ISSUE_LOG) {

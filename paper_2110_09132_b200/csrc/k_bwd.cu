@@ -277,6 +277,7 @@ __device__ __forceinline__ void emit_rows(const DevCtx& c, int p, const float* r
 #endif
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+  EMB_TR_ENTRY();
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float smem_f[];
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(3, t);
   const int* cnt = counts_of(c, p, r);
   const int U = cnt[CNT_U], NCH = cnt[CNT_NCH];
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -378,14 +380,17 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx
       __syncthreads();
     }
   }
+  EMB_TR_END(3, t);
   pdl_trigger();
 }
 
 // ------------------------------------------------------------------ scheduled push (N > 1)
 __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
+  EMB_TR_ENTRY();
   pdl_wait();
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(5, t);
   const int U = counts_of(c, p, r)[CNT_U];
   const int* uid = c.uid + pn(c, p, r) * (size_t)c.max_tok;
   const size_t row_bytes = (size_t)c.D * c.esz, slice_bytes = (size_t)c.d * c.esz;
@@ -398,6 +403,7 @@ __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
     const int s = c16 / c.cps, cs = c16 - s * c.cps;
     st16(recv_of(c, s, p, r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
   }
+  EMB_TR_END(5, t);
   pdl_trigger();
 }
 
@@ -427,9 +433,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t t = c.t_rec[p];
-  if (blockIdx.x == 0 && threadIdx.x == 0) publish(c, EMB_FLAG_OFF(pub[0]), t);  // rawpush completed
-  if (threadIdx.x == 0) wait_all(c, flags_of(c, c.r)->pub[0], t);
-  __syncthreads();
+  (void)t;  // N > 1: every rawpush completed (the gate before this kernel waited for the pub flags)
   int nchs[EMB_WMAX];
   int total = 0;
 #pragma unroll
@@ -512,16 +516,13 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p)
 // are summed in ascending source rank, then scaled and applied.
 template <int DT, bool RAWSRC>
 __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int part, int G) {
+  EMB_TR_ENTRY();
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   const uint32_t t = c.t_rec[p];
-  if (!RAWSRC) {
-    // the sender pass that precedes this kernel on this stream has completed
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-      publish(c, part ? EMB_FLAG_OFF(pub[1]) : EMB_FLAG_OFF(pub[0]), t);
-    if (threadIdx.x == 0) wait_all(c, flags_of(c, c.r)->pub[part], t);
-    __syncthreads();
-  }
+  EMB_TR_BEGIN(part ? 6 : 4, t);
+  // N > 1: every sender's pass of this part completed (the gate before this
+  // kernel waited for their pub flags)
   int cnt[EMB_WMAX];
   int total = 0;
 #pragma unroll
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       st16(wp, Vec<DT>::pack(w));
     }
   }
+  EMB_TR_END(part ? 6 : 4, t);
   pdl_trigger();
 }
 

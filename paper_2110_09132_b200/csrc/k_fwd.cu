@@ -26,8 +26,11 @@ static constexpr int FWD_ROWS = 4;  // rows in flight per warp
 template <int V>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* __restrict__ ids, int n,
                                                           char* __restrict__ out, int p, int prefetched) {
+  EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
+  EMB_TR_BEGIN(0, t);
+  EMB_TR_AT(0, t, 4);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
   if (tid == 0) {
@@ -37,12 +40,8 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       const double td = (double)t;
       c.alpha[p] = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
     }
-    // the main stream has completed merge(prior, t-1) and (via the host's event
-    // wait) merge(scheduled, t-2): publish them (see kernels.cuh protocol)
-    if (t >= 2) publish(c, EMB_FLAG_OFF(prior_done), t - 1);
-    const uint32_t dd = (c.mode == SPLIT) ? t - 2 : t - 1;
-    if ((int)dd >= 1) publish(c, EMB_FLAG_OFF(def_done), dd);
     for (int s = 0; s < c.N; ++s) atomicAdd(&c.stats[s], (unsigned long long)n * c.d * c.esz);
+    EMB_TR_MID(0, t);
   }
   // (a1) all-gather of this rank's ids into every peer's gids[p][r] (published by route)
   if (!prefetched) {
@@ -59,13 +58,8 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       if (mine[j] != ids[j]) atomicOr(c.err, ERR_STATE);
     if (tid == 0 && *ntok_of(c, c.r, p, c.r) != n) atomicOr(c.err, ERR_STATE);
   }
-  // wait: every owner applied the prior part of t-1 and the scheduled part of t-2
-  if (threadIdx.x == 0) {
-    Flags* f = flags_of(c, c.r);
-    wait_all(c, f->prior_done, t - 1);
-    wait_all(c, f->def_done, t - 2);
-  }
-  __syncthreads();
+  // every owner applied the prior part of t-1 and the scheduled part of t-2:
+  // the gate before this kernel (N > 1) waited for their flags
 
   // (a2-a4) pull-gather: warp per row; lane holds 16-byte chunks c16 = lane + 32 v
   const int lane = threadIdx.x & 31;
@@ -107,6 +101,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       }
     }
   }
+  EMB_TR_END(0, t);
   pdl_trigger();
 }
 

@@ -1,0 +1,78 @@
+// k_gate.cu — the peer-flag gates of the N > 1 exchange (DESIGN.md "Flag
+// protocol", "Liveness").
+//
+// Every cross-GPU wait of the path happens in a gate: ONE CTA of one warp,
+// launched on the stream right before the kernel that consumes the peers'
+// data.  The gate (a) starts after its stream predecessor completed
+// (griddepcontrol.wait), so that producer's stores are performed, and
+// publishes the producer's flag to every peer; (b) spins until every peer's
+// matching flag arrived; (c) only then lets its dependent launch
+// (griddepcontrol.launch_dependents after the wait).  The compute kernels
+// themselves never spin.
+//
+// Why a separate kernel: a wide kernel whose CTAs spin occupies SMs while it
+// waits, and two such kernels on different streams of two GPUs can starve the
+// very kernels their peers wait for (observed: a side-stream merge spinning on
+// every SM of one GPU while the other GPU's forward spun on every SM — a
+// cross-GPU deadlock, EMB_ERR_TIMEOUT).  Gates hold one warp while waiting, so
+// every other kernel can always be scheduled and every wait eventually
+// resolves.  The only other spinning kernel is mark (N <= 8 CTAs).
+#include <stddef.h>
+
+#include "kernels.cuh"
+
+namespace emb {
+
+__global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int flag_arg) {
+  EMB_TR_ENTRY();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    switch (kind) {
+      case GATE_FWD: {
+        // forward(t): the main stream completed merge(prior, t-1) and (host event)
+        // merge(scheduled, t-2); every owner must have done the same
+        const uint32_t t = c.t_rec[p ^ 1] + 1;
+        EMB_TR_BEGIN(10 + kind, t);
+        const uint32_t dd = (c.mode == SPLIT) ? t - 2 : t - 1;
+        publish2(c, EMB_FLAG_OFF(prior_done), t - 1, t >= 2, EMB_FLAG_OFF(def_done), dd, (int)dd >= 1);
+        Flags* f = flags_of(c, c.r);
+        wait_all(c, f->prior_done, t - 1);
+        wait_all(c, f->def_done, t - 2);
+        EMB_TR_END(10 + kind, t);
+        break;
+      }
+      case GATE_SORT: {
+        // sort of batch tt: every source's ids must be here.  flag_arg = 1: the
+        // forward (this stream's event predecessor) pushed this rank's ids.
+        const uint32_t tt = c.t_rec[p ^ 1] + 1;
+        EMB_TR_BEGIN(10 + kind, tt);
+        if (flag_arg) publish(c, EMB_FLAG_OFF(ids), tt);
+        wait_all(c, flags_of(c, c.r)->ids, tt);
+        EMB_TR_END(10 + kind, tt);
+        break;
+      }
+      case GATE_PUB0:
+      case GATE_PUB1: {
+        // owner merge of part (prior / scheduled): the sender pass preceding this
+        // gate completed; every sender's pass must have completed
+        const uint32_t t = c.t_rec[p];
+        EMB_TR_BEGIN(10 + kind, t);
+        const int part = (kind == GATE_PUB1) ? 1 : 0;
+        publish(c, part ? EMB_FLAG_OFF(pub[1]) : EMB_FLAG_OFF(pub[0]), t);
+        wait_all(c, flags_of(c, c.r)->pub[part], t);
+        EMB_TR_END(10 + kind, t);
+        break;
+      }
+      default:
+        atomicOr(c.err, ERR_STATE);
+    }
+  }
+  __syncwarp();
+  pdl_trigger();  // after the wait: the dependent's CTAs must not launch (and sit) earlier
+}
+
+cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s) {
+  return launch_pdl(gate_kernel, dim3(1), dim3(32), 0, s, c, p, kind, flag_arg);
+}
+
+}  // namespace emb

@@ -96,6 +96,7 @@ __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {
 // ============================================================== sort (aux stream)
 template <typename K, int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, int fwd_pushed) {
+  EMB_TR_ENTRY();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int kb = (c.max_tok + 1 + 3) & ~3;  // keys per buffer (+1 for segs[U]), 16-byte aligned
@@ -112,10 +113,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   // pushed there) or after mark(t-1) (prefetched) — possibly before forward(t)
   // wrote t_rec[p] — so derive it from the previous iteration's record.
   const uint32_t tt = c.t_rec[p ^ 1] + 1;
-  EMB_TS(20);
-  if (n == 0 && tid == 0 && fwd_pushed) publish(c, EMB_FLAG_OFF(ids), tt);
-  if (tid == 0 && c.N > 1) wait_flag(c, &flags_of(c, c.r)->ids[n], tt);
-  __syncthreads();
+  EMB_TR_BEGIN(1, tt);
+  (void)fwd_pushed;  // N > 1: the gate before this kernel published / waited the ids flags
 
   const int T = __ldcg(ntok_of(c, c.r, p, n));
   const int* g = gids_of(c, c.r, p, n);
@@ -146,7 +145,6 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
     }
   }
   __syncthreads();
-  EMB_TS(21);
 
   // LSD radix passes over [posbits, dshift + 1): blocked keys, private counters
   const int b0 = tid * EPT;
@@ -199,7 +197,6 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
     __syncthreads();
     K* sw = keyA; keyA = keyB; keyB = sw;
   }
-  EMB_TS(22);
 
   // ---- heads -> unique kept ids (ascending), segments, owner routing
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
@@ -255,7 +252,6 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
     kbase += __popc(keptm);
   }
   __syncthreads();
-  EMB_TS(23);
 
   // ---- reduce chunks (C rows) per unique, chunk -> unique, multi-chunk list
   int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
@@ -312,7 +308,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
     cn[CNT_NCH] = NCH;
     cn[CNT_NLONG] = NLONG;
   }
-  EMB_TS(24);
+  EMB_TR_END(1, tt);
   pdl_trigger();
 }
 
@@ -322,39 +318,64 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
 // CTAs wait for every rank's next ids and tag D_next: nextmark[p][id] = t+1.
 __global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* __restrict__ next_ids, int n_next,
                                                     int do_mark) {
+  EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(2, t);
   const int p1 = p ^ 1;
   const int tid = threadIdx.x;
+  constexpr int MK = 16;  // ids per thread in flight: max_tok <= 16 * 1024
   if (next_ids != nullptr) {
+    int v[MK];
+#pragma unroll
+    for (int k = 0; k < MK; ++k) {
+      const int j = tid + k * 1024;
+      v[k] = (j < n_next) ? __ldg(next_ids + j) : 0;
+    }
     for (int s = blockIdx.x; s < c.N; s += gridDim.x) {
       int* dst = gids_of(c, s, p1, c.r);
-      for (int j = tid; j < n_next; j += blockDim.x) dst[j] = __ldg(next_ids + j);
+#pragma unroll
+      for (int k = 0; k < MK; ++k) {
+        const int j = tid + k * 1024;
+        if (j < n_next) dst[j] = v[k];
+      }
       if (tid == 0) {
         *ntok_of(c, s, p1, c.r) = n_next;
         atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n_next * 4ull);
       }
       __syncthreads();
+      EMB_TR_AT(2, t, 4);
       if (tid == 0 && c.N > 1) {
-        __threadfence_system();
-        st_release_sys(&flags_of(c, s)->ids[c.r], t + 1);
+        fence_acq_rel_sys();  // cumulative over the CTA's stores (ordered by the barrier)
+        EMB_TR_AT(2, t, 5);
+        st_relaxed_sys(&flags_of(c, s)->ids[c.r], t + 1);
       }
     }
   }
+  EMB_TR_MID(2, t);
   if (do_mark && next_ids != nullptr) {
     if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1);  // grid = N CTAs: co-resident
     __syncthreads();
+    EMB_TR_WAITED(2, t);
     int* mark = c.nextmark + (size_t)p * c.L;
     const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
     for (int s = 0; s < c.N; ++s) {
       const int cn = __ldcg(ntok_of(c, c.r, p1, s));
       const int* gn = gids_of(c, c.r, p1, s);
-      for (int j = gtid; j < cn; j += nthr) {
-        const int id = __ldcg(gn + j);
-        if ((unsigned)id < (unsigned long long)c.L) mark[id] = (int)(t + 1);
+      for (int j0 = gtid; j0 < cn; j0 += MK * nthr) {
+        int id[MK];
+#pragma unroll
+        for (int k = 0; k < MK; ++k) {
+          const int j = j0 + k * nthr;
+          id[k] = (j < cn) ? __ldcg(gn + j) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < MK; ++k)
+          if ((unsigned)id[k] < (unsigned long long)c.L) mark[id[k]] = (int)(t + 1);
       }
     }
   }
+  EMB_TR_END(2, t);
   pdl_trigger();
 }
 
@@ -363,6 +384,7 @@ __global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* 
 // D_n = U_n \ P_n ascending (a stable ballot partition of the unique ids).
 template <int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) {
+  EMB_TR_ENTRY();
   pdl_wait();
   __shared__ int s_tmp[64];
   __shared__ int s_tot[2];
@@ -370,6 +392,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(9, t);
   const int U = counts_of(c, p, n)[CNT_U];
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
   const int* uid = c.uid + bpn;
@@ -406,6 +429,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) 
     dbase += __popc(dm);
   }
   if (tid == 0) c.counts[pn(c, p, n) * CNT_W + CNT_P] = P_tot;
+  EMB_TR_END(9, t);
   pdl_trigger();
 }
 

@@ -39,10 +39,10 @@ inline cudaError_t launch_pdl_raw(const void* f, dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelExC(&cfg, f, args);
 }
 
-// Flag publication protocol (DESIGN.md "Synchronisation"): a kernel never
-// fences its own stores; the NEXT kernel on the same stream (or one ordered
-// after it by an event), which starts only after the producer completed,
-// publishes the producer's flag to every peer (one thread, one system fence),
+// Flag publication protocol (DESIGN.md "Flag protocol"): a kernel never
+// fences its own stores; the gate that follows it on the same stream (or is
+// ordered after it by an event) starts only after the producer completed,
+// publishes the producer's flag to every peer (relaxed system-scope stores),
 // then waits for the peers' flags.  N == 1 skips the protocol (stream order).
 //
 // Rows of the backward are addressed by the sender's UNIQUE index i (the
@@ -50,6 +50,11 @@ inline cudaError_t launch_pdl_raw(const void* f, dim3 grid, dim3 block, size_t s
 // scheduled is an epoch-tagged mark of D_next that every kernel tests per id,
 // so no prefix over the split sits on the critical path.  The slot-ordered
 // Alg. 1 tables (P_n, D_n) are produced off the critical path (tables).
+
+// Peer-flag gates (k_gate.cu): every N > 1 cross-GPU wait runs in a one-warp
+// kernel right before the consumer; compute kernels never spin.
+enum GateKind { GATE_FWD = 0, GATE_SORT = 1, GATE_PUB0 = 2, GATE_PUB1 = 3 };
+cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s);
 
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
 // id push or prefetch check, wait for every owner, pull-gather)
