@@ -54,7 +54,7 @@ typedef struct CUevent_st* emb_event_t;   /* == cudaEvent_t  */
 typedef enum {
   EMB_OK = 0,
   EMB_ERR_INVALID_ARG = 1, /* NULL / negative / unknown enum                        */
-  EMB_ERR_SHAPE = 2,       /* D % N != 0, (D/N)*e % 16 != 0, N > D, N > 8            */
+  EMB_ERR_SHAPE = 2,       /* D % N != 0, (D/N)*e % 16 != 0, N > D, N > 8, D > 1024 */
   EMB_ERR_ID_RANGE = 3,    /* a token id < 0 or >= L (device-detected, sticky)       */
   EMB_ERR_CAPACITY = 4,    /* n > max_tokens, or the per-source sort does not fit     */
   EMB_ERR_STATE = 5,       /* call order; ids of forward(t+1) != next_ids of bwd(t)  */
@@ -121,7 +121,8 @@ typedef enum {
   EMB_K_RAWCOAL = 8,  /* RAW owner-side coalesce                                  */
   EMB_K_TABLES = 9,   /* a8 Alg. 1 slot tables P_n ++ D_n (off the critical path) */
   EMB_K_GATE = 10,    /* N > 1 peer-flag gate (one warp: publish + wait)           */
-  EMB_NUM_KERNELS = 11
+  EMB_K_APPLY = 11,   /* a7 combine + a9/a10 push (N > 1) or a11 update (N == 1)   */
+  EMB_NUM_KERNELS = 12
 } emb_kernel_kind;
 
 /* Debug items for emb_debug_copy (integer parity tests). `src` selects the
@@ -188,7 +189,10 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
  *              `out` (same n and ids); borrowed until `stream` completes
  *   next_ids : device int32 [n_next], the ids this rank will pass to the next
  *              forward (the paper's prefetch), or NULL on the
- *              last step (D_next = empty: every row is scheduled, reading R8)
+ *              last step (D_next = empty: every row is scheduled, reading R8).
+ *              Borrowed: it may be read by the library's streams until the
+ *              NEXT emb_backward_exchange call; writes to it must be ordered
+ *              on `stream` after that call.
  * Every shard row in U = unique(all ranks' ids, pad dropped if pad_id >= 0)
  * receives one optimizer step with g = grad_scale * sum over ranks of its dY
  * rows.  SPLIT: rows in D_next are updated on `stream`; the rest on the side

@@ -71,12 +71,13 @@ struct DevCtx {
   int* uid;               // [2][N][max_tok]    ascending unique kept ids
   int* useg;              // [2][N][max_tok+1]  unique i -> first index into perm (useg[U] = end)
   int* chunk_off;         // [2][N][max_tok+1]  unique i -> first reduce chunk
-  int* chunk_uidx;        // [2][N][max_chunks] chunk -> unique i
+  int4* chunk_desc;       // [2][N][max_chunks] chunk -> {unique i, perm begin, perm end, chunks of i}
   int* long_u;            // [2][N][max_long]   uniques with more than one chunk
   int* slot_id;           // [2][N][max_tok]    Alg. 1 slot order (prior asc, then scheduled asc) — tables
   int* counts;            // [2][N][CNT_W]
   float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
-  int* slot_ctr;          // [2][N][max_tok]    chunk arrivals of multi-chunk uniques (re-armed to 0)
+  int* slot_ctr;          // [2][N][max_tok]    (unused; reserved)
+  float* gcoal;           // [max_tok][D] fp32  sender-coalesced rows of single-chunk uniques (COAL/SPLIT)
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
   unsigned int* t_rec;    // [2]   t of the iteration using parity p

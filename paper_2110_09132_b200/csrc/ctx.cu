@@ -57,7 +57,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if ((pl->d * pl->esz) % 16 != 0) return EMB_ERR_SHAPE;
   pl->cpr = cfg->dim * pl->esz / 16;
   pl->cps = pl->d * pl->esz / 16;
-  if (pl->cpr > 256) return EMB_ERR_SHAPE;  // rows up to 4 KB
+  if (pl->cpr > 256 || cfg->dim > 1024) return EMB_ERR_SHAPE;  // rows up to 4 KB; fp32 sums of D <= 1024
   pl->C = 16;
   pl->max_chunks = cfg->max_tokens + cfg->max_tokens / pl->C + 1;
   pl->max_long = cfg->max_tokens / (pl->C + 1) + 1;
@@ -82,7 +82,8 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (N > 1) loc += 2 * L * N * 8;                               // slotmap
   loc += 2 * L * 4;                                              // nextmark
   loc += 5 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id slot_ctr | useg chunk_off
-  loc += 2 * N * (size_t)pl->max_chunks * 4 + 2 * N * CNT_W * 4 + 2 * N * (size_t)pl->max_long * 4;
+  loc += 2 * N * (size_t)pl->max_chunks * 16 + 2 * N * CNT_W * 4 + 2 * N * (size_t)pl->max_long * 4;
+  if (cfg->mode != EMB_BWD_RAW) loc += T * cfg->dim * 4;       // gcoal
   loc += 2 * (size_t)pl->max_chunks * cfg->dim * 4;              // scratch
   if (cfg->mode == EMB_BWD_SPLIT && N > 1) loc += 2 * T * cfg->dim * pl->esz;
   if (cfg->mode == EMB_BWD_RAW) loc += 2 * N * T * pl->d * 4;
@@ -104,11 +105,12 @@ struct emb_ctx {
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // per-source sort of the next batch (overlaps the current iteration)
-  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {};
+  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
+  bool tables_pending[2] = {false, false};  // N == 1: tables(t) on the side stream still reads parity t&1
   cudaEvent_t ev_marked = nullptr, ev_join_aux = nullptr, ev_join_side = nullptr;
-  bool mark_pending = false;  // N == 1: mark runs on aux; the next forward checks its pushed ids
+  bool mark_pending = false;  // N == 1: mark runs on the side stream; the next forward checks its pushed ids
   bool aux_used = false, side_used = false;  // since the last emb_join
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
@@ -249,7 +251,8 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.useg, 2 * N * (T + 1) * 4);
     ALLOC(c.slot_id, 2 * N * T * 4);
     ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
-    ALLOC(c.chunk_uidx, 2 * N * (size_t)pl.max_chunks * 4);
+    ALLOC(c.chunk_desc, 2 * N * (size_t)pl.max_chunks * 16);
+    if (cfg->mode != EMB_BWD_RAW) ALLOC(c.gcoal, T * cfg->dim * 4);
     ALLOC(c.long_u, 2 * N * (size_t)pl.max_long * 4);
     ALLOC(c.slot_ctr, 2 * N * T * 4);
     ALLOC(c.counts, 2 * N * CNT_W * 4);
@@ -275,6 +278,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cudaEventCreateWithFlags(&ctx->ev_def[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_main[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_sorted[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+    if (cudaEventCreateWithFlags(&ctx->ev_tables[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
   }
   if (cudaEventCreateWithFlags(&ctx->ev_marked, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_aux, cudaEventDisableTiming) != cudaSuccess) goto fail;
@@ -368,7 +372,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->it += 1;
   const int p = (int)(ctx->it & 1);
   if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
-  if (ctx->mark_pending) {  // N == 1: the prefetch push ran on the aux stream
+  if (ctx->mark_pending) {  // N == 1: the prefetch copy ran on the side stream
     CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_marked, 0));
     ctx->mark_pending = false;
   }
@@ -382,7 +386,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     CKC(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_main[p], 0));
     CKC(ctx, gate(ctx, p, GATE_SORT, 1, ctx->aux));
     CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux, [&] {
-      return launch_sort(ctx->dc, p, 1, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
+      return launch_sort(ctx->dc, p, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
     }));
     CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], ctx->aux));
     ctx->sort_pending[p] = true;
@@ -412,32 +416,55 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   cudaStream_t aux = ctx->aux;
   const int N = ctx->pl.N;
   const int do_mark = (mode == EMB_BWD_SPLIT && next_ids) ? 1 : 0;
-  // a5: prefetch all-gather of the next ids + D_next marks.  N > 1 the owners
-  // need the marks before the coalesce (prior rows travel first): main stream.
-  // N == 1 nothing on the critical path needs them (the coalesce applies every
-  // row; the split only feeds the tables): aux stream, overlapping the coalesce.
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));  // caller's next_ids / dY are ready in stream order
-  cudaStream_t ms = (N > 1) ? stream : aux;
-  if (N == 1) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
-  CKC(ctx, run_k(ctx, EMB_K_ROUTE, ms, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, ms); }));
   if (N == 1) {
-    CKC(ctx, cudaEventRecord(ctx->ev_marked, aux));
+    // N == 1: nothing on the critical path needs the D_next marks (the coalesce
+    // applies every row), so
+    //   aux:  a6 for the next batch straight from the caller's next_ids, one
+    //         iteration ahead and first in line (the coalesce of t+1 waits for it);
+    //   side: a5 (ids copy for the forward's prefetch check + D_next marks) and
+    //         the a8 slot tables of this batch.
+    // next_ids is read asynchronously until the next backward (header contract).
+    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
+    if (next_ids) {
+      if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_tables[p ^ 1], 0));
+      CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
+        return launch_sort(c, p ^ 1, next_ids, n_next, ctx->pl.key64, ctx->pl.sort_smem, aux);
+      }));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
+      ctx->sort_pending[p ^ 1] = true;
+      ctx->tables_pending[p ^ 1] = false;
+    }
+    CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_main[p], 0));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, side); }));
+    CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
     ctx->mark_pending = true;
+    if (ctx->sort_pending[p]) CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_sorted[p], 0));
+    CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, side); }));
+    CKC(ctx, cudaEventRecord(ctx->ev_tables[p], side));
+    ctx->tables_pending[p] = true;
+    ctx->side_used = true;
+    ctx->aux_used = true;
   } else {
+    // a5: prefetch all-gather of the next ids + D_next marks: the owners need
+    // the marks before the coalesce (prior rows travel first): main stream.
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, stream, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, stream); }));
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
     CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
-  }
-  ctx->aux_used = true;
-  // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
-  CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
-  if (next_ids) {
-    // a6 for the next batch, one iteration ahead.  Its parity's previous user
-    // (the scheduled merge of t-1) must be done with the routing tables.
-    if (ctx->def_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_def[p ^ 1], 0));
-    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 0, aux));
-    CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] { return launch_sort(c, p ^ 1, 0, ctx->pl.key64, ctx->pl.sort_smem, aux); }));
-    CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
-    ctx->sort_pending[p ^ 1] = true;
+    ctx->aux_used = true;
+    // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
+    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
+    if (next_ids) {
+      // a6 for the next batch, one iteration ahead.  Its parity's previous user
+      // (the scheduled merge of t-1) must be done with the routing tables.
+      if (ctx->def_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_def[p ^ 1], 0));
+      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 0, aux));
+      CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
+        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
+      }));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
+      ctx->sort_pending[p ^ 1] = true;
+    }
   }
   if (ctx->sort_pending[p]) {  // the sort of this batch (aux stream) must be complete
     CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
@@ -450,6 +477,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
+    CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.
     if (ctx->pl.N > 1) {
@@ -546,6 +574,7 @@ emb_status emb_join(emb_ctx* ctx, emb_stream_t stream_) {
   for (int p = 0; p < 2; ++p) {
     ctx->def_pending[p] = false;
     ctx->sort_pending[p] = false;
+    ctx->tables_pending[p] = false;
   }
   ctx->mark_pending = false;
   return EMB_OK;
@@ -718,6 +747,7 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_def[i]) cudaEventDestroy(ctx->ev_def[i]);
     if (ctx->ev_main[i]) cudaEventDestroy(ctx->ev_main[i]);
     if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
+    if (ctx->ev_tables[i]) cudaEventDestroy(ctx->ev_tables[i]);
   }
   for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side}) {
     if (e) cudaEventDestroy(e);

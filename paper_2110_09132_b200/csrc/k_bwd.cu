@@ -264,123 +264,175 @@ __device__ __forceinline__ void emit_rows(const DevCtx& c, int p, const float* r
 }
 
 // ------------------------------------------------------------------ sender coalesce
-// CTA b takes 8 consecutive chunks per round (one per warp).  Each warp
-// reduces its chunk (<= C rows, ascending position, fp32).  A single-chunk
-// unique's row is parked in shared memory and the CTA emits the parked rows
-// together.  Chunks of multi-chunk (Zipf-head) uniques leave fp32 partials;
-// the CTA then adds its chunk count to the unique's arrival counter, and the
-// CTA completing a unique combines all of its partials (warps sum contiguous
-// partial ranges, then a fixed-order shared-memory combine — deterministic
-// whichever CTA arrives last) and emits it.
-#ifndef EMB_COAL_MINB
-#define EMB_COAL_MINB 1  // 2 forces 128 registers and spills: measured 1.7x slower (round 1)
-#endif
+// Two kernels, so that neither needs a CTA barrier on its hot loop:
+//  coal_reduce  warp per reduce chunk (<= C rows of one unique, ascending
+//               position), fp32 sums in registers: a single-chunk unique's sum
+//               goes to gcoal[i], a multi-chunk (Zipf-head) unique's chunk sums
+//               to scratch.  No shared memory, no barriers: the occupancy is
+//               what hides the perm -> dY load chain.
+//  coal_apply   (1) CTA per multi-chunk unique: its chunk sums are combined in
+//               a fixed order (warps sum contiguous ranges, then a fixed warp-
+//               order shared-memory sum: deterministic) and emitted by the
+//               CTA; (2) thread per (single-chunk unique, 16-byte wire chunk):
+//               N == 1 the optimizer step in place (one source = the merged
+//               gradient), N > 1 the wire-rounded slice stored into the
+//               owner's receive row i over NVLink (prior) or the stage
+//               (scheduled).  Every load of an item is issued before its math.
 template <int DT, int V>
-__global__ void __launch_bounds__(BWD_THREADS, EMB_COAL_MINB) coal_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+__global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+  EMB_TR_ENTRY();
+  pdl_wait();
+  constexpr int EPV = Vec<DT>::EPV;
+  const int r = c.r;
+  const uint32_t t = c.t_rec[p];
+  (void)t;
+  EMB_TR_BEGIN(3, t);
+  const int NCH = counts_of(c, p, r)[CNT_NCH];
+  const int4* desc = c.chunk_desc + pn(c, p, r) * (size_t)c.max_chunks;
+  const int* perm = c.perm + pn(c, p, r) * (size_t)c.max_tok;
+  float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
+  const size_t row_bytes = (size_t)c.D * c.esz;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int ch = gw; ch < NCH; ch += nw) {
+    const int4 dsc = desc[ch];  // {unique i, perm begin, perm end, chunks of i}
+    float acc[V * EPV];
+    reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, dsc.y, dsc.z, acc);
+    store_partial<EPV, V>((dsc.w > 1) ? part + (size_t)ch * c.D : c.gcoal + (size_t)dsc.x * c.D, c.cpr, acc);
+  }
+  EMB_TR_END(3, t);
+  pdl_trigger();
+}
+
+#ifndef EMB_APPLY_MINB
+#define EMB_APPLY_MINB 2
+#endif
+template <int DT, int V>  // V: float4 columns of an fp32 row per lane, D / 4 <= 32 V
+__global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float smem_f[];
-  float* rows = smem_f;                        // [BWD_WARPS][D] parked single-chunk rows / combined row
-  float* comb = smem_f + BWD_WARPS * c.D;      // [BWD_WARPS][D] warp partials of a long unique
-  __shared__ int s_k[BWD_WARPS], s_n[BWD_WARPS], s_last[BWD_WARPS], s_ks[BWD_WARPS], s_us[BWD_WARPS],
-      s_pr[BWD_WARPS];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* row = smem_f;              // [D]            combined row of a multi-chunk unique
+  float* comb = smem_f + c.D;       // [BWD_WARPS][D] warp partial sums
+  __shared__ int s_k[1], s_u[1], s_pr[1];
+  const int w = threadIdx.x >> 5;
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
-  EMB_TR_BEGIN(3, t);
+  EMB_TR_BEGIN(15, t);
   const int* cnt = counts_of(c, p, r);
-  const int U = cnt[CNT_U], NCH = cnt[CNT_NCH];
+  const int U = cnt[CNT_U], NLONG = cnt[CNT_NLONG];
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int s = 0; s < c.N; ++s) atomicAdd(&c.stats[c.N + s], (unsigned long long)U * c.d * c.esz);
   const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;
   const size_t bpn = pn(c, p, r) * (size_t)c.max_tok;
-  const int* perm = c.perm + bpn;
   const int* uid = c.uid + bpn;
-  const int* useg = c.useg + pn(c, p, r) * (size_t)(c.max_tok + 1);
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
-  const int* chunk_uidx = c.chunk_uidx + pn(c, p, r) * (size_t)c.max_chunks;
-  int* slot_ctr = c.slot_ctr + bpn;
-  float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
-  const size_t row_bytes = (size_t)c.D * c.esz;
-  for (int base = blockIdx.x * BWD_WARPS; base < NCH; base += gridDim.x * BWD_WARPS) {
-    const int ch = base + w;
-    int k = -1, nch = 0;
+  const int* long_u = c.long_u + pn(c, p, r) * (size_t)c.max_long;
+  const float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
+  const int ncol4 = c.D / 4;  // float4 columns of an fp32 row
+
+  // (1) multi-chunk uniques: one CTA each
+  for (int lu = blockIdx.x; lu < NLONG; lu += gridDim.x) {
+    const int kk = long_u[lu];
+    const int c0 = chunk_off[kk], n2 = chunk_off[kk + 1] - c0;
+    const int q0 = c0 + (int)((long long)n2 * w / BWD_WARPS), q1 = c0 + (int)((long long)n2 * (w + 1) / BWD_WARPS);
     {
-      float acc[V * EPV];
-      if (ch < NCH) {
-        k = chunk_uidx[ch];
-        const int c0 = chunk_off[k];
-        nch = chunk_off[k + 1] - c0;
-        const int b = useg[k] + (ch - c0) * c.C;
-        const int e = min(useg[k + 1], b + c.C);
-        reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, b, e, acc);
-        store_partial<EPV, V>((nch > 1) ? part + (size_t)ch * c.D : rows + (size_t)w * c.D, c.cpr, acc);
-      }
-    }
-    if (lane == 0) {
-      const bool single = (ch < NCH && nch == 1);
-      s_k[w] = (nch > 1) ? k : -1;
-      s_ks[w] = single ? k : -1;
-      const int id = single ? uid[k] : 0;
-      s_us[w] = id;
-      s_pr[w] = single && (c.N == 1 || is_prior(c, p, t, id));
-      s_last[w] = -1;
+      float acc[V * 4];
+      sum_partials<4, V>(part, c.D, ncol4, q0, q1, acc);
+      store_partial<4, V>(comb + (size_t)w * c.D, ncol4, acc);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      // distinct multi-chunk uniques of this round (their chunks are consecutive)
-      int nd = 0;
-      for (int i = 0; i < BWD_WARPS; ++i) {
-        if (s_k[i] < 0) continue;
-        if (nd > 0 && s_k[i] == s_last[nd - 1]) { s_n[nd - 1]++; continue; }
-        s_last[nd] = s_k[i];
-        s_n[nd] = 1;
-        ++nd;
-      }
-      __threadfence();  // this round's partials before the arrival counts
-      for (int i = 0; i < nd; ++i) {
-        const int kk = s_last[i];
-        const int tot = chunk_off[kk + 1] - chunk_off[kk];
-        const int prev = atomicAdd(&slot_ctr[kk], s_n[i]);
-        if (prev + s_n[i] == tot) slot_ctr[kk] = 0;  // complete here; re-arm for the next use
-        else s_last[i] = -1;                          // another CTA will combine it
-      }
-      for (int i = nd; i < BWD_WARPS; ++i) s_last[i] = -1;
-      __threadfence();
-    }
-    __syncthreads();
-    emit_rows<DT>(c, p, rows, s_ks, s_us, s_pr, BWD_WARPS, alpha);
-    __syncthreads();
-    for (int i = 0; i < BWD_WARPS; ++i) {
-      const int kk = s_last[i];
-      if (kk < 0) continue;
-      const int c0 = chunk_off[kk], n2 = chunk_off[kk + 1] - c0;
-      const int q0 = c0 + (int)((long long)n2 * w / BWD_WARPS), q1 = c0 + (int)((long long)n2 * (w + 1) / BWD_WARPS);
-      {
-        float acc[V * EPV];
-        sum_partials<EPV, V>(part, c.D, c.cpr, q0, q1, acc);
-        store_partial<EPV, V>(comb + (size_t)w * c.D, c.cpr, acc);
-      }
-      __syncthreads();
-      for (int x = threadIdx.x; x < c.D; x += blockDim.x) {  // fixed warp order
-        float sum = 0.f;
+    for (int x = threadIdx.x; x < c.D; x += blockDim.x) {  // fixed warp order
+      float sum = 0.f;
 #pragma unroll
-        for (int ww = 0; ww < BWD_WARPS; ++ww) sum += comb[(size_t)ww * c.D + x];
-        rows[x] = sum;
+      for (int ww = 0; ww < BWD_WARPS; ++ww) sum += comb[(size_t)ww * c.D + x];
+      row[x] = sum;
+    }
+    if (threadIdx.x == 0) {
+      const int id = uid[kk];
+      s_k[0] = kk;
+      s_u[0] = id;
+      s_pr[0] = (c.N == 1 || is_prior(c, p, t, id));
+    }
+    __syncthreads();
+    emit_rows<DT>(c, p, row, s_k, s_u, s_pr, 1, alpha);
+    __syncthreads();
+  }
+
+  // (2) single-chunk uniques: thread per (unique i, 16-byte wire chunk)
+  constexpr int EA = (EPV == 4) ? 2 : 1;  // items in flight per thread
+  const int total = U * c.cpr;
+  const int stride = gridDim.x * blockDim.x;
+  const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
+  const bool adam = (c.optim == ADAM);
+  char* shard = shard_of(c, r);
+  for (int b0 = blockIdx.x * blockDim.x + threadIdx.x; b0 < total; b0 += stride * EA) {
+    int kk[EA], cc[EA], id[EA];
+    bool ok[EA];
+    float g[EA][EPV];
+    uint4 wr[EA];
+    float mm[EA][EPV], vv[EA][EPV];
+#pragma unroll
+    for (int j = 0; j < EA; ++j) {
+      const int it = b0 + j * stride;
+      kk[j] = it / c.cpr;
+      cc[j] = it - kk[j] * c.cpr;
+      ok[j] = it < total && (chunk_off[kk[j] + 1] - chunk_off[kk[j]]) == 1;
+      id[j] = ok[j] ? uid[kk[j]] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < EA; ++j) {
+      if (!ok[j]) continue;
+      const float* gp = c.gcoal + (size_t)kk[j] * c.D + cc[j] * EPV;
+#pragma unroll
+      for (int x = 0; x < EPV; x += 4) {
+        const float4 g4 = __ldcg(reinterpret_cast<const float4*>(gp + x));
+        g[j][x] = g4.x; g[j][x + 1] = g4.y; g[j][x + 2] = g4.z; g[j][x + 3] = g4.w;
       }
-      if (threadIdx.x == 0) {
-        const int id = uid[kk];
-        s_ks[0] = kk;
-        s_us[0] = id;
-        s_pr[0] = (c.N == 1 || is_prior(c, p, t, id));
+      if (c.N == 1) {
+        const size_t u = (size_t)id[j];
+        wr[j] = ld16(shard + u * slice_bytes + (size_t)cc[j] * 16);
+        if (adam) {
+#pragma unroll
+          for (int x = 0; x < EPV; x += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + cc[j] * EPV + x);
+            const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + cc[j] * EPV + x);
+            mm[j][x] = m4.x; mm[j][x + 1] = m4.y; mm[j][x + 2] = m4.z; mm[j][x + 3] = m4.w;
+            vv[j][x] = v4.x; vv[j][x + 1] = v4.y; vv[j][x + 2] = v4.z; vv[j][x + 3] = v4.w;
+          }
+        }
       }
-      __syncthreads();
-      emit_rows<DT>(c, p, rows, s_ks, s_us, s_pr, 1, alpha);
-      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < EA; ++j) {
+      if (!ok[j]) continue;
+      const uint4 gw8 = Vec<DT>::pack(g[j]);  // wire rounding point (reading R11)
+      if (c.N == 1) {
+        const size_t u = (size_t)id[j];
+        float gr[EPV], wv[EPV];
+        Vec<DT>::unpack(gw8, gr);
+        Vec<DT>::unpack(wr[j], wv);
+        opt_math<EPV>(c, alpha, gr, wv, mm[j], vv[j]);
+        st16(shard + u * slice_bytes + (size_t)cc[j] * 16, Vec<DT>::pack(wv));
+        if (adam) {
+#pragma unroll
+          for (int x = 0; x < EPV; x += 4) {
+            *reinterpret_cast<float4*>(c.adam_m + u * c.d + cc[j] * EPV + x) =
+                make_float4(mm[j][x], mm[j][x + 1], mm[j][x + 2], mm[j][x + 3]);
+            *reinterpret_cast<float4*>(c.adam_v + u * c.d + cc[j] * EPV + x) =
+                make_float4(vv[j][x], vv[j][x + 1], vv[j][x + 2], vv[j][x + 3]);
+          }
+        }
+      } else if (is_prior(c, p, t, id[j])) {
+        const int s = cc[j] / c.cps, cs = cc[j] - s * c.cps;
+        st16(recv_of(c, s, p, r) + (size_t)kk[j] * slice_bytes + (size_t)cs * 16, gw8);
+      } else {
+        st16(c.stage + ((size_t)p * c.max_tok + kk[j]) * row_bytes + (size_t)cc[j] * 16, gw8);
+      }
     }
   }
-  EMB_TR_END(3, t);
+  EMB_TR_END(15, t);
   pdl_trigger();
 }
 
@@ -449,13 +501,9 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
     for (int m = 0; m < EMB_WMAX - 1; ++m)
       if (n == m && ch >= nchs[m]) { ch -= nchs[m]; n = m + 1; }
     const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
-    const int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
-    const int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
-    const int k = c.chunk_uidx[pn(c, p, n) * (size_t)c.max_chunks + ch];
-    const int c0 = chunk_off[k], nch = chunk_off[k + 1] - c0;
-    const int b = useg[k] + (ch - c0) * c.C;
-    const int e = min(useg[k + 1], b + c.C);
-    reduce_rows<DT, V, true>(recv_of(c, c.r, p, n), slice_bytes, c.cps, c.perm + bpn, b, e, acc);
+    const int4 dsc = c.chunk_desc[pn(c, p, n) * (size_t)c.max_chunks + ch];  // {k, begin, end, nch}
+    const int k = dsc.x, nch = dsc.w;
+    reduce_rows<DT, V, true>(recv_of(c, c.r, p, n), slice_bytes, c.cps, c.perm + bpn, dsc.y, dsc.z, acc);
     float* dst = (nch > 1) ? c.scratch + (size_t)p * c.max_chunks * c.D + ((size_t)n * c.max_chunks + ch) * c.d
                            : c.gc_owner + (bpn + k) * (size_t)c.d;
     store_partial<EPV, V>(dst, c.cps, acc);
@@ -634,21 +682,38 @@ static int grid_for_warps(long long warps, int cap) {
                : cudaErrorInvalidValue)
 
 template <int DT>
-static void coal_smem(int V, size_t smem) {
-  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if (V <= 1) cudaFuncSetAttribute(coal_kernel<DT, 1>, a, (int)smem);
-  else if (V <= 2) cudaFuncSetAttribute(coal_kernel<DT, 2>, a, (int)smem);
-  else if (V <= 4) cudaFuncSetAttribute(coal_kernel<DT, 4>, a, (int)smem);
-  else cudaFuncSetAttribute(coal_kernel<DT, 8>, a, (int)smem);
+static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
+  const int V = (c.cpr + 31) / 32;
+  const int ga = grid_for_warps(c.max_chunks, L.nsm * 12);
+  return EMB_LAUNCH_V(V, coal_reduce_kernel, DT, ga, 0, c, y, p);
 }
 
 template <int DT>
-static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
-  const int V = (c.cpr + 31) / 32;
-  const int ga = grid_for_warps(c.max_chunks, L.nsm * 8);
-  const size_t smem = (size_t)2 * BWD_WARPS * c.D * 4;
-  if (smem > 48 * 1024) coal_smem<DT>(V, smem);
-  return EMB_LAUNCH_V(V, coal_kernel, DT, ga, smem, c, y, p);
+static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
+  constexpr int EA = (Vec<DT>::EPV == 4) ? 2 : 1;
+  const long long items = (long long)c.max_tok * c.cpr;
+  long long grid = (items + (long long)BWD_THREADS * EA - 1) / ((long long)BWD_THREADS * EA);
+  if (grid > L.nsm * 8) grid = L.nsm * 8;
+  if (grid < 1) grid = 1;
+  const size_t smem = (size_t)(1 + BWD_WARPS) * c.D * 4;
+  const int V = (c.D / 4 + 31) / 32;
+  if (V <= 2) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(coal_apply_kernel<DT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return launch_pdl(coal_apply_kernel<DT, 2>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
+  }
+  if (V <= 4) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(coal_apply_kernel<DT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return launch_pdl(coal_apply_kernel<DT, 4>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(coal_apply_kernel<DT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return launch_pdl(coal_apply_kernel<DT, 8>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
+}
+
+cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
+  return c.dtype == BF16 ? apply_dispatch<BF16>(c, L, p, s) : apply_dispatch<F32>(c, L, p, s);
 }
 
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s) {

@@ -95,7 +95,7 @@ __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {
 
 // ============================================================== sort (aux stream)
 template <typename K, int EPT>
-__global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, int fwd_pushed) {
+__global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, const int* own_ids, int own_n) {
   EMB_TR_ENTRY();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -114,10 +114,12 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   // wrote t_rec[p] — so derive it from the previous iteration's record.
   const uint32_t tt = c.t_rec[p ^ 1] + 1;
   EMB_TR_BEGIN(1, tt);
-  (void)fwd_pushed;  // N > 1: the gate before this kernel published / waited the ids flags
+  // N > 1: the gate before this kernel published / waited the ids flags.
+  // own_ids (N == 1 prefetch): this rank's batch is read straight from the caller.
 
-  const int T = __ldcg(ntok_of(c, c.r, p, n));
-  const int* g = gids_of(c, c.r, p, n);
+  const bool own = own_ids != nullptr && n == c.r;
+  const int T = own ? own_n : __ldcg(ntok_of(c, c.r, p, n));
+  const int* g = own ? own_ids : gids_of(c, c.r, p, n);
   const int posbits = c.posbits, idbits = c.idbits;
   const int dshift = posbits + idbits;
   const long long L = c.L;
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   }
   __syncthreads();
 
+  EMB_TR_AT(1, tt, 4);
   // LSD radix passes over [posbits, dshift + 1): blocked keys, private counters
   const int b0 = tid * EPT;
   const int topbit = dshift + 1;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
     K* sw = keyA; keyA = keyB; keyB = sw;
   }
 
+  EMB_TR_AT(1, tt, 5);
   // ---- heads -> unique kept ids (ascending), segments, owner routing
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
   int* perm = c.perm + bpn;
@@ -253,9 +257,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
   }
   __syncthreads();
 
+  EMB_TR_AT(1, tt, 6);
   // ---- reduce chunks (C rows) per unique, chunk -> unique, multi-chunk list
   int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
-  int* chunk_uidx = c.chunk_uidx + pn(c, p, n) * (size_t)c.max_chunks;
+  int4* chunk_desc = c.chunk_desc + pn(c, p, n) * (size_t)c.max_chunks;
   int* long_u = c.long_u + pn(c, p, n) * (size_t)c.max_long;
   const int per_w = (U + RT_WARPS - 1) / RT_WARPS;
   const int k0w = min(U, w * per_w), k1w = min(U, k0w + per_w);
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) sort_kernel(DevCtx c, int p, in
         const int off = cb + incl - nch;
         useg[k] = a;
         chunk_off[k] = off;
-        for (int q = 0; q < nch; ++q) chunk_uidx[off + q] = k;
+        for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
         if (nch > 1) long_u[lb + __popc(longm & lt_mask)] = k;
       }
       cb += __shfl_sync(0xffffffffu, incl, 31);
@@ -479,11 +484,12 @@ cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem) {
   return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size_t smem, cudaStream_t s) {
+cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
+                        cudaStream_t s) {
   void* f = key64 ? sort_fn<unsigned long long>(ept_for(c.max_tok)) : sort_fn<uint32_t>(ept_for(c.max_tok));
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
-  void* args[] = {&cc, &p, &fwd_pushed};
+  void* args[] = {&cc, &p, &own_ids, &own_n};
   return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), smem, s, args);
 }
 

@@ -62,7 +62,8 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
                        int prefetched, cudaStream_t s);
 // a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
 // owner routing (slotmap) — auxiliary stream, one iteration ahead
-cudaError_t launch_sort(const DevCtx& c, int p, int fwd_pushed, bool key64, size_t smem, cudaStream_t s);
+cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
+                        cudaStream_t s);
 size_t sort_smem_bytes(int max_tok, bool key64);
 cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
 // a5: prefetch all-gather of the next ids + D_next epoch marks (Alg. 1 line 4's set)
@@ -75,6 +76,8 @@ cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s);
 // applies the optimizer directly, N > 1 pushes prior rows to the owners and
 // stages scheduled rows.
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s);
+// a7 (multi-chunk combine) + a9/a10 or the N == 1 update: coalesced rows -> owners / stage / shard
+cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
 // a12: push the staged scheduled rows to their owners (N > 1)
 cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
 // RAW a7/a10: push raw dY column slices; owner-side per-source coalesce

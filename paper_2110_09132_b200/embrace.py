@@ -62,7 +62,7 @@ class EmbStats(ctypes.Structure):
 
 
 KERNEL_NAMES = ["fwd_pull_gather", "sort_unique", "mark_next", "coal_push", "merge_update_prior",
-                "defpush", "merge_update_sched", "rawpush", "rawcoal", "split_tables", "peer_gate"]
+                "defpush", "merge_update_sched", "rawpush", "rawcoal", "split_tables", "peer_gate", "coal_apply"]
 EMB_NUM_KERNELS = len(KERNEL_NAMES)
 
 
