@@ -54,13 +54,15 @@ def _stale(lib, srcs):
 
 def build(force=False, verbose=False):
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    if not force and not _stale(LIB, srcs):
+    extra = os.environ.get("EMB_NVCC_EXTRA", "").split()  # e.g. -DEMB_TRACE (kernel trace builds)
+    stamp = LIB + ".flags"
+    same_flags = os.path.exists(stamp) and open(stamp).read() == " ".join(extra)
+    if not force and same_flags and not _stale(LIB, srcs):
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     inc, libdir = _nccl_dirs()
     nvcc = _nvcc()
     common = ARCH + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", inc]
-    extra = os.environ.get("EMB_NVCC_EXTRA", "").split()  # e.g. -DEMB_PHASE_TIMING (profiling builds)
     common += extra
 
     def comp(src):
@@ -83,6 +85,8 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-4000:])
     os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(" ".join(extra))
     if verbose:
         print("built", LIB)
     return LIB
