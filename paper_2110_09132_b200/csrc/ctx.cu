@@ -13,6 +13,10 @@
 
 #include "../../include/embrace.h"
 #include "common.cuh"
+
+#ifndef EMB_C
+#define EMB_C 16
+#endif
 #include "dense_queue.h"
 #include "kernels.cuh"
 
@@ -58,12 +62,12 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   pl->cpr = cfg->dim * pl->esz / 16;
   pl->cps = pl->d * pl->esz / 16;
   if (pl->cpr > 256 || cfg->dim > 1024) return EMB_ERR_SHAPE;  // rows up to 4 KB; fp32 sums of D <= 1024
-  pl->C = 16;
+  pl->C = EMB_C;  // rows per sender reduce chunk (B5)
   pl->max_chunks = cfg->max_tokens + cfg->max_tokens / pl->C + 1;
   pl->max_long = cfg->max_tokens / (pl->C + 1) + 1;
   pl->idbits = bits_for(cfg->vocab);  // the value L itself is the invalid-id sentinel
   pl->posbits = bits_for(cfg->max_tokens - 1);
-  pl->key64 = 1 + pl->idbits + pl->posbits > 32;  // dropped bit | id | pos
+  pl->key64 = pl->idbits + pl->posbits > 32;  // (id or sentinel L) | pos
   pl->sort_smem = sort_smem_bytes(cfg->max_tokens, pl->key64);
   if (pl->sort_smem > 227 * 1024) return EMB_ERR_CAPACITY;
 

@@ -40,7 +40,7 @@ static constexpr int BWD_WARPS = BWD_THREADS / 32;
 // Rows in flight per warp in the segmented reduce.  Most uniques have 1-2 rows
 // (Zipf tail), so 2 in flight costs little latency and saves load registers.
 #ifndef EMB_RB
-#define EMB_RB 2
+#define EMB_RB 4
 #endif
 
 // acc[v*EPV + i] = sum over rows perm[b..e) (ascending) of row[c16 = lane + 32 v]
@@ -305,18 +305,74 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
 }
 
 #ifndef EMB_APPLY_MINB
-#define EMB_APPLY_MINB 2
+#define EMB_APPLY_MINB 3
 #endif
-template <int DT, int V>  // V: float4 columns of an fp32 row per lane, D / 4 <= 32 V
+// One 16-byte wire chunk c16 of coalesced row k (id, merged fp32 g): loads of
+// the state first (apply_load), then the math and stores (apply_store).
+//   N == 1: optimizer step in place (SGD / Adam, opt_math);
+//   N > 1:  the wire-rounded slice goes to the owner's receive row k (prior,
+//           NVLink store) or to the stage (scheduled).
+template <int DT>
+struct ApplyState {
+  uint4 w;
+  float m[Vec<DT>::EPV], v[Vec<DT>::EPV];
+};
+template <int DT>
+__device__ __forceinline__ void apply_load(const DevCtx& c, int id, int c16, ApplyState<DT>& st) {
+  constexpr int EPV = Vec<DT>::EPV;
+  if (c.N != 1) return;
+  const size_t u = (size_t)id;
+  st.w = ld16(shard_of(c, c.r) + u * ((size_t)c.d * c.esz) + (size_t)c16 * 16);
+  if (c.optim == ADAM) {
+#pragma unroll
+    for (int x = 0; x < EPV; x += 4) {
+      const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + c16 * EPV + x);
+      const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + c16 * EPV + x);
+      st.m[x] = m4.x; st.m[x + 1] = m4.y; st.m[x + 2] = m4.z; st.m[x + 3] = m4.w;
+      st.v[x] = v4.x; st.v[x + 1] = v4.y; st.v[x + 2] = v4.z; st.v[x + 3] = v4.w;
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ void apply_store(const DevCtx& c, int p, uint32_t t, int k, int id, int c16, const float* g,
+                                            ApplyState<DT>& st, float alpha) {
+  constexpr int EPV = Vec<DT>::EPV;
+  const uint4 gw = Vec<DT>::pack(g);  // wire rounding point (reading R11)
+  const size_t slice_bytes = (size_t)c.d * c.esz;
+  if (c.N == 1) {
+    const size_t u = (size_t)id;
+    float gr[EPV], wv[EPV];
+    Vec<DT>::unpack(gw, gr);
+    Vec<DT>::unpack(st.w, wv);
+    opt_math<EPV>(c, alpha, gr, wv, st.m, st.v);
+    st16(shard_of(c, c.r) + u * slice_bytes + (size_t)c16 * 16, Vec<DT>::pack(wv));
+    if (c.optim == ADAM) {
+#pragma unroll
+      for (int x = 0; x < EPV; x += 4) {
+        *reinterpret_cast<float4*>(c.adam_m + u * c.d + c16 * EPV + x) =
+            make_float4(st.m[x], st.m[x + 1], st.m[x + 2], st.m[x + 3]);
+        *reinterpret_cast<float4*>(c.adam_v + u * c.d + c16 * EPV + x) =
+            make_float4(st.v[x], st.v[x + 1], st.v[x + 2], st.v[x + 3]);
+      }
+    }
+  } else if (is_prior(c, p, t, id)) {
+    const int s = c16 / c.cps, cs = c16 - s * c.cps;
+    st16(recv_of(c, s, p, c.r) + (size_t)k * slice_bytes + (size_t)cs * 16, gw);
+  } else {
+    st16(c.stage + ((size_t)p * c.max_tok + k) * ((size_t)c.D * c.esz) + (size_t)c16 * 16, gw);
+  }
+}
+
+static constexpr int SLICE = 128;  // fp32 columns per combine slice (one float4 per lane)
+
+template <int DT>
 __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
-  extern __shared__ __align__(16) float smem_f[];
-  float* row = smem_f;              // [D]            combined row of a multi-chunk unique
-  float* comb = smem_f + c.D;       // [BWD_WARPS][D] warp partial sums
-  __shared__ int s_k[1], s_u[1], s_pr[1];
-  const int w = threadIdx.x >> 5;
+  __shared__ __align__(16) float comb[BWD_WARPS][SLICE];  // warp partial sums of one column slice
+  __shared__ __align__(16) float row[SLICE];              // combined slice
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
   EMB_TR_BEGIN(15, t);
@@ -330,106 +386,88 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
   const int* long_u = c.long_u + pn(c, p, r) * (size_t)c.max_long;
   const float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
-  const int ncol4 = c.D / 4;  // float4 columns of an fp32 row
 
-  // (1) multi-chunk uniques: one CTA each
-  for (int lu = blockIdx.x; lu < NLONG; lu += gridDim.x) {
+  // (1) multi-chunk (Zipf-head) uniques, split into (unique, 128-column slice)
+  //     items so that a huge segment (e.g. the pad id) is combined by many
+  //     CTAs: warps sum contiguous ranges of chunk partials (ascending, 8 loads
+  //     in flight), then a fixed warp-order sum — deterministic.
+  const int NS = (c.D + SLICE - 1) / SLICE;
+  for (int item = blockIdx.x; item < NLONG * NS; item += gridDim.x) {
+    const int lu = item / NS, sl = item - lu * NS;
     const int kk = long_u[lu];
     const int c0 = chunk_off[kk], n2 = chunk_off[kk + 1] - c0;
     const int q0 = c0 + (int)((long long)n2 * w / BWD_WARPS), q1 = c0 + (int)((long long)n2 * (w + 1) / BWD_WARPS);
-    {
-      float acc[V * 4];
-      sum_partials<4, V>(part, c.D, ncol4, q0, q1, acc);
-      store_partial<4, V>(comb + (size_t)w * c.D, ncol4, acc);
+    const int col = sl * SLICE + lane * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col < c.D) {
+      for (int q = q0; q < q1; q += 8) {
+        float4 b[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          b[j] = (q + j < q1) ? __ldcg(reinterpret_cast<const float4*>(part + (size_t)(q + j) * c.D + col))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc.x += b[j].x; acc.y += b[j].y; acc.z += b[j].z; acc.w += b[j].w;
+        }
+      }
     }
+    *reinterpret_cast<float4*>(&comb[w][lane * 4]) = acc;
     __syncthreads();
-    for (int x = threadIdx.x; x < c.D; x += blockDim.x) {  // fixed warp order
+    if (threadIdx.x < SLICE) {
       float sum = 0.f;
 #pragma unroll
-      for (int ww = 0; ww < BWD_WARPS; ++ww) sum += comb[(size_t)ww * c.D + x];
-      row[x] = sum;
-    }
-    if (threadIdx.x == 0) {
-      const int id = uid[kk];
-      s_k[0] = kk;
-      s_u[0] = id;
-      s_pr[0] = (c.N == 1 || is_prior(c, p, t, id));
+      for (int ww = 0; ww < BWD_WARPS; ++ww) sum += comb[ww][threadIdx.x];
+      row[threadIdx.x] = sum;
     }
     __syncthreads();
-    emit_rows<DT>(c, p, row, s_k, s_u, s_pr, 1, alpha);
+    if (threadIdx.x < SLICE / EPV) {
+      const int c16 = sl * (SLICE / EPV) + threadIdx.x;
+      if (c16 < c.cpr) {
+        const int id = uid[kk];
+        ApplyState<DT> st;
+        apply_load<DT>(c, id, c16, st);
+        float g[EPV];
+#pragma unroll
+        for (int x = 0; x < EPV; ++x) g[x] = row[threadIdx.x * EPV + x];
+        apply_store<DT>(c, p, t, kk, id, c16, g, st, alpha);
+      }
+    }
     __syncthreads();
   }
 
-  // (2) single-chunk uniques: thread per (unique i, 16-byte wire chunk)
-  constexpr int EA = (EPV == 4) ? 2 : 1;  // items in flight per thread
-  const int total = U * c.cpr;
-  const int stride = gridDim.x * blockDim.x;
-  const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
-  const bool adam = (c.optim == ADAM);
-  char* shard = shard_of(c, r);
-  for (int b0 = blockIdx.x * blockDim.x + threadIdx.x; b0 < total; b0 += stride * EA) {
-    int kk[EA], cc[EA], id[EA];
-    bool ok[EA];
-    float g[EA][EPV];
-    uint4 wr[EA];
-    float mm[EA][EPV], vv[EA][EPV];
+  // (2) single-chunk uniques: RPB rows per CTA pass, thread = one 16-byte wire
+  //     chunk (the (row, chunk) split is computed once: no division in the loop)
+  constexpr int EA = (EPV == 4) ? 2 : 1;  // rows in flight per thread
+  const int RPB = BWD_THREADS / c.cpr;
+  const int rl = threadIdx.x / c.cpr, c16 = threadIdx.x - rl * c.cpr;
+  if (rl < RPB) {
+    const int step = gridDim.x * RPB;
+    for (int k0 = blockIdx.x * RPB + rl; k0 < U; k0 += step * EA) {
+      int kk[EA], id[EA];
+      bool ok[EA];
+      float g[EA][EPV];
+      ApplyState<DT> st[EA];
 #pragma unroll
-    for (int j = 0; j < EA; ++j) {
-      const int it = b0 + j * stride;
-      kk[j] = it / c.cpr;
-      cc[j] = it - kk[j] * c.cpr;
-      ok[j] = it < total && (chunk_off[kk[j] + 1] - chunk_off[kk[j]]) == 1;
-      id[j] = ok[j] ? uid[kk[j]] : 0;
-    }
-#pragma unroll
-    for (int j = 0; j < EA; ++j) {
-      if (!ok[j]) continue;
-      const float* gp = c.gcoal + (size_t)kk[j] * c.D + cc[j] * EPV;
-#pragma unroll
-      for (int x = 0; x < EPV; x += 4) {
-        const float4 g4 = __ldcg(reinterpret_cast<const float4*>(gp + x));
-        g[j][x] = g4.x; g[j][x + 1] = g4.y; g[j][x + 2] = g4.z; g[j][x + 3] = g4.w;
+      for (int j = 0; j < EA; ++j) {
+        kk[j] = k0 + j * step;
+        ok[j] = kk[j] < U && (chunk_off[kk[j] + 1] - chunk_off[kk[j]]) == 1;
+        id[j] = ok[j] ? uid[kk[j]] : 0;
       }
-      if (c.N == 1) {
-        const size_t u = (size_t)id[j];
-        wr[j] = ld16(shard + u * slice_bytes + (size_t)cc[j] * 16);
-        if (adam) {
 #pragma unroll
-          for (int x = 0; x < EPV; x += 4) {
-            const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + cc[j] * EPV + x);
-            const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + cc[j] * EPV + x);
-            mm[j][x] = m4.x; mm[j][x + 1] = m4.y; mm[j][x + 2] = m4.z; mm[j][x + 3] = m4.w;
-            vv[j][x] = v4.x; vv[j][x + 1] = v4.y; vv[j][x + 2] = v4.z; vv[j][x + 3] = v4.w;
-          }
+      for (int j = 0; j < EA; ++j) {
+        if (!ok[j]) continue;
+        const float* gp = c.gcoal + (size_t)kk[j] * c.D + c16 * EPV;
+#pragma unroll
+        for (int x = 0; x < EPV; x += 4) {
+          const float4 g4 = __ldcg(reinterpret_cast<const float4*>(gp + x));
+          g[j][x] = g4.x; g[j][x + 1] = g4.y; g[j][x + 2] = g4.z; g[j][x + 3] = g4.w;
         }
+        apply_load<DT>(c, id[j], c16, st[j]);
       }
-    }
 #pragma unroll
-    for (int j = 0; j < EA; ++j) {
-      if (!ok[j]) continue;
-      const uint4 gw8 = Vec<DT>::pack(g[j]);  // wire rounding point (reading R11)
-      if (c.N == 1) {
-        const size_t u = (size_t)id[j];
-        float gr[EPV], wv[EPV];
-        Vec<DT>::unpack(gw8, gr);
-        Vec<DT>::unpack(wr[j], wv);
-        opt_math<EPV>(c, alpha, gr, wv, mm[j], vv[j]);
-        st16(shard + u * slice_bytes + (size_t)cc[j] * 16, Vec<DT>::pack(wv));
-        if (adam) {
-#pragma unroll
-          for (int x = 0; x < EPV; x += 4) {
-            *reinterpret_cast<float4*>(c.adam_m + u * c.d + cc[j] * EPV + x) =
-                make_float4(mm[j][x], mm[j][x + 1], mm[j][x + 2], mm[j][x + 3]);
-            *reinterpret_cast<float4*>(c.adam_v + u * c.d + cc[j] * EPV + x) =
-                make_float4(vv[j][x], vv[j][x + 1], vv[j][x + 2], vv[j][x + 3]);
-          }
-        }
-      } else if (is_prior(c, p, t, id[j])) {
-        const int s = cc[j] / c.cps, cs = cc[j] - s * c.cps;
-        st16(recv_of(c, s, p, r) + (size_t)kk[j] * slice_bytes + (size_t)cs * 16, gw8);
-      } else {
-        st16(c.stage + ((size_t)p * c.max_tok + kk[j]) * row_bytes + (size_t)cc[j] * 16, gw8);
-      }
+      for (int j = 0; j < EA; ++j)
+        if (ok[j]) apply_store<DT>(c, p, t, kk[j], id[j], c16, g[j], st[j], alpha);
     }
   }
   EMB_TR_END(15, t);
@@ -691,25 +729,11 @@ static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char
 template <int DT>
 static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
   constexpr int EA = (Vec<DT>::EPV == 4) ? 2 : 1;
-  const long long items = (long long)c.max_tok * c.cpr;
-  long long grid = (items + (long long)BWD_THREADS * EA - 1) / ((long long)BWD_THREADS * EA);
+  const int rpb = BWD_THREADS / c.cpr;
+  long long grid = ((long long)c.max_tok + (long long)rpb * EA - 1) / ((long long)rpb * EA);
   if (grid > L.nsm * 8) grid = L.nsm * 8;
   if (grid < 1) grid = 1;
-  const size_t smem = (size_t)(1 + BWD_WARPS) * c.D * 4;
-  const int V = (c.D / 4 + 31) / 32;
-  if (V <= 2) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(coal_apply_kernel<DT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(coal_apply_kernel<DT, 2>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
-  }
-  if (V <= 4) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(coal_apply_kernel<DT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(coal_apply_kernel<DT, 4>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
-  }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(coal_apply_kernel<DT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(coal_apply_kernel<DT, 8>, dim3((int)grid), dim3(BWD_THREADS), smem, s, c, p);
+  return launch_pdl(coal_apply_kernel<DT>, dim3((int)grid), dim3(BWD_THREADS), 0, s, c, p);
 }
 
 cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {

@@ -1,0 +1,374 @@
+// k_sort.cu — a6 of SURVEY §8(a): per-source sort / unique / reduce chunks /
+// owner routing, one thread-block CLUSTER per source.
+//
+// PAPER.md:380 (§4.2.2): "The calculations require a considerable computing
+// resource, and the GPU idle time after BP is a good occasion"; Alg. 1
+// line 2 D_u = UNIQUE(D_cur[n]) and COALESCE(G) need, per
+// source n, the ascending unique ids and the positions of each id in
+// ascending position order (reading R12: canonical summation order).
+//
+// B200 design (DESIGN.md §5 "sort_unique").  A batch of up to 16384 keys is
+// too little work for 148 SMs and too much for one: one SM needed 22 us (LM)
+// to 62 us (BERT), enough to bound the whole step from the auxiliary stream.
+// Here a cluster of CL = 8 CTAs shares one source's keys through distributed
+// shared memory (DSMEM):
+//   keys   (id' << posbits) | pos with id' = L for dropped tokens (pad when
+//          pad_id >= 0, out-of-range ids), so dropped keys sort last; a
+//          stable LSD radix sort over the id bits only (8-bit digits: LM 3
+//          passes, 32K vocabularies 2) keeps equal ids in position order.
+//   pass   every CTA ranks its slice (warp match_any ranking into per-warp
+//          digit counters), publishes its 256-bin histogram, reads the other
+//          CTAs' histograms over DSMEM to get each digit's global start, and
+//          scatters every key straight into the destination CTA's shared
+//          memory (global position P -> CTA P / S, slot P % S).
+//   heads  kept segment heads are counted per CTA, offset across the cluster
+//          over DSMEM, and written as uid / useg / perm / slotmap; then the
+//          reduce chunks (C rows) of every unique, the chunk descriptors, and
+//          the multi-chunk (Zipf-head) list, again offset over DSMEM.
+// Nine cluster barriers per sort (LM), no global atomics, deterministic.
+#include <cooperative_groups.h>
+#include <stddef.h>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace emb {
+
+static constexpr int CL = 8;           // CTAs per cluster (portable size)
+static constexpr int CS_THREADS = 256;
+static constexpr int CS_WARPS = CS_THREADS / 32;
+static constexpr int NB = 256;         // bins of an 8-bit digit
+static constexpr int DB = 8;
+
+// Exclusive scan of one int per thread over the CTA (CS_THREADS); *total gets the sum.
+__device__ __forceinline__ int cta_exscan(int v, int* tmp, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  int wsum = 0, all = 0;
+#pragma unroll
+  for (int i = 0; i < CS_WARPS; ++i) {
+    const int ti = tmp[i];
+    if (i < w) wsum += ti;
+    all += ti;
+  }
+  *total = all;
+  __syncthreads();
+  return wsum + x - v;
+}
+
+// Sum of `v` over the cluster's CTAs with rank < cr (exclusive) and over all.
+__device__ __forceinline__ void cluster_exsum(cg::cluster_group& cluster, int* slot, int cr, int* before, int* all) {
+  int b = 0, a = 0;
+#pragma unroll
+  for (int q = 0; q < CL; ++q) {
+    const int x = *cluster.map_shared_rank(slot, q);
+    if (q < cr) b += x;
+    a += x;
+  }
+  *before = b;
+  *all = a;
+}
+
+template <typename K, int EPT>
+__global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, const int* own_ids, int own_n) {
+  EMB_TR_ENTRY();
+  pdl_wait();
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int SMAX = EPT * CS_THREADS;  // keys per CTA slice (max)
+  constexpr int EPW = EPT * 32;           // keys per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* keyA = reinterpret_cast<K*>(smem_raw);
+  K* keyB = keyA + SMAX;
+  __shared__ int wh[CS_WARPS][NB];  // per-warp digit counts -> exclusive warp offsets
+  __shared__ int ch[NB];            // this CTA's digit totals (read by the cluster)
+  __shared__ int gs[NB];            // global start of (digit, this CTA)
+  __shared__ int tmp[CS_WARPS];
+  __shared__ int xs[4];             // values exchanged over DSMEM: kept heads, kept tokens, chunks, long
+  __shared__ int wk[CS_WARPS];
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int cr = (int)cluster.block_rank();
+  const int n = blockIdx.x / CL;  // source
+  const uint32_t tt = c.t_rec[p ^ 1] + 1;  // iteration of the batch (see sort note in k_route.cu history)
+  EMB_TR_BEGIN(1, tt);
+  // N > 1: the gate before this kernel published / waited the ids flags.
+  // own_ids (N == 1 prefetch): this rank's batch is read straight from the caller.
+  const bool own = own_ids != nullptr && n == c.r;
+  const int T = own ? own_n : __ldcg(ntok_of(c, c.r, p, n));
+  const int* g = own ? own_ids : gids_of(c, c.r, p, n);
+  const int S = (T + CL - 1) / CL;  // slice of each CTA (<= SMAX: T <= max_tok <= CL * SMAX)
+  const int lo = cr * S;
+  const int cnt = max(0, min(T, lo + S) - lo);
+  const int posbits = c.posbits, idbits = c.idbits;
+  const long long L = c.L;
+
+  // ---- load: key = (id' << posbits) | pos, id' = L for dropped tokens (reading R6)
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = tid + e * CS_THREADS;
+    if (i < cnt) {
+      const int gi = lo + i;
+      const int id = __ldcg(g + gi);
+      long long idp = id;
+      if ((unsigned)id >= (unsigned long long)L) idp = L;               // invalid (the forward flags it)
+      else if (c.pad_id >= 0 && (long long)id == c.pad_id) idp = L;     // pad: no gradient
+      keyA[i] = (K(idp) << posbits) | K(gi);
+    }
+  }
+  __syncthreads();
+
+  // ---- stable LSD radix over the id bits, 8-bit digits, scatter through DSMEM
+  const int top = posbits + idbits;
+  for (int sh = posbits; sh < top; sh += DB) {
+    const unsigned dmask = (1u << min(DB, top - sh)) - 1u;
+#pragma unroll
+    for (int j = 0; j < NB / 32; ++j) wh[w][lane + 32 * j] = 0;
+    __syncwarp();
+    K kk[EPT];
+    int dg[EPT], rk[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = w * EPW + r * 32 + lane;
+      const bool valid = i < cnt;
+      const unsigned act = __ballot_sync(0xffffffffu, valid);
+      dg[r] = 0;
+      if (valid) {
+        kk[r] = keyA[i];
+        dg[r] = (int)((unsigned)(kk[r] >> sh) & dmask);
+        const unsigned peers = __match_any_sync(act, dg[r]);
+        const int base = wh[w][dg[r]];
+        rk[r] = base + __popc(peers & lt);
+        __syncwarp(act);
+        if (lane == __ffs(peers) - 1) wh[w][dg[r]] = base + __popc(peers);
+        __syncwarp(act);
+      }
+    }
+    __syncthreads();
+    {  // digit d = tid: exclusive offsets over warps, CTA total
+      int run = 0;
+#pragma unroll
+      for (int ww = 0; ww < CS_WARPS; ++ww) {
+        const int x = wh[ww][tid];
+        wh[ww][tid] = run;
+        run += x;
+      }
+      ch[tid] = run;
+    }
+    cluster.sync();  // every CTA's ch[] is complete
+    {
+      int pre, tot, all;
+      cluster_exsum(cluster, &ch[tid], cr, &pre, &tot);
+      const int ex = cta_exscan(tot, tmp, &all);
+      gs[tid] = ex + pre;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = w * EPW + r * 32 + lane;
+      if (i < cnt) {
+        const int P = gs[dg[r]] + wh[w][dg[r]] + rk[r];
+        const int dst = P / S;
+        *cluster.map_shared_rank(keyB + (P - dst * S), dst) = kk[r];
+      }
+    }
+    cluster.sync();  // scatters landed; nobody reads ch[] / keyA any more
+    K* sw = keyA; keyA = keyB; keyB = sw;
+  }
+
+  // ---- heads -> unique kept ids (ascending), segments, owner routing
+  const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
+  int* perm = c.perm + bpn;
+  int* uid = c.uid + bpn;
+  int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
+  const K posmask = (K(1) << posbits) - 1;
+  K prev_last = K(0);
+  if (cr > 0 && cnt > 0) prev_last = *cluster.map_shared_rank(keyA + (S - 1), cr - 1);
+  int kept_heads = 0, kept_tok = 0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = w * EPW + r * 32 + lane;
+    const bool valid = i < cnt;
+    bool head = false, keep = false;
+    if (valid) {
+      const K key = keyA[i];
+      const long long idp = (long long)(key >> posbits);
+      keep = idp < L;
+      const K prev = (i > 0) ? keyA[i - 1] : prev_last;
+      head = keep && ((i == 0 && cr == 0) || (prev >> posbits) != (key >> posbits));
+    }
+    kept_heads += __popc(__ballot_sync(0xffffffffu, head));
+    kept_tok += __popc(__ballot_sync(0xffffffffu, valid && keep));
+  }
+  if (lane == 0) wk[w] = kept_heads;
+  {
+    int tk_all;
+    const int tk_ex = cta_exscan(lane == 0 ? kept_tok : 0, tmp, &tk_all);
+    (void)tk_ex;
+    if (tid == 0) xs[1] = tk_all;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int ww = 0; ww < CS_WARPS; ++ww) { const int x = wk[ww]; wk[ww] = run; run += x; }
+    xs[0] = run;
+  }
+  cluster.sync();  // xs[0] (kept heads) and xs[1] (kept tokens) of every CTA
+  int kb, U, tkb, Tk;
+  cluster_exsum(cluster, &xs[0], cr, &kb, &U);
+  cluster_exsum(cluster, &xs[1], cr, &tkb, &Tk);
+  (void)tkb;
+  {
+    int kbase = kb + wk[w];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = w * EPW + r * 32 + lane;
+      const bool valid = i < cnt;
+      bool head = false;
+      K key = K(0);
+      if (valid) {
+        key = keyA[i];
+        const bool keep = (long long)(key >> posbits) < L;
+        const K prev = (i > 0) ? keyA[i - 1] : prev_last;
+        head = keep && ((i == 0 && cr == 0) || (prev >> posbits) != (key >> posbits));
+      }
+      const unsigned hm = __ballot_sync(0xffffffffu, head);
+      if (valid) {
+        perm[lo + i] = (int)(key & posmask);
+        if (head) {
+          const int k = kbase + __popc(hm & lt);
+          const int id = (int)(key >> posbits);
+          uid[k] = id;
+          useg[k] = lo + i;
+          if (c.N > 1) c.slotmap[((size_t)p * c.L + id) * c.N + n] = ((unsigned long long)tt << 32) | (unsigned)k;
+        }
+      }
+      kbase += __popc(hm);
+    }
+  }
+  if (cr == 0 && tid == 0) useg[U] = Tk;  // end of the last kept segment (kept keys sort first)
+  cluster.sync();  // useg[] of the whole cluster is in global memory (release / acquire at cluster scope)
+
+  // ---- reduce chunks of C rows per unique: descriptors, multi-chunk list
+  int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
+  int4* chunk_desc = c.chunk_desc + pn(c, p, n) * (size_t)c.max_chunks;
+  int* long_u = c.long_u + pn(c, p, n) * (size_t)c.max_long;
+  const int hc = xs[0];  // this CTA's uniques: [kb, kb + hc)
+  int my_ch = 0, my_long = 0;
+  for (int j = tid; j < hc; j += CS_THREADS) {
+    const int k = kb + j;
+    const int nch = (__ldcg(useg + k + 1) - __ldcg(useg + k) + c.C - 1) / c.C;
+    my_ch += nch;
+    my_long += nch > 1;
+  }
+  {
+    int a, b;
+    cta_exscan(my_ch, tmp, &a);
+    cta_exscan(my_long, tmp, &b);
+    if (tid == 0) { xs[2] = a; xs[3] = b; }
+  }
+  cluster.sync();
+  int cb, NCH, lb, NLONG;
+  cluster_exsum(cluster, &xs[2], cr, &cb, &NCH);
+  cluster_exsum(cluster, &xs[3], cr, &lb, &NLONG);
+  for (int j0 = 0; j0 < hc; j0 += CS_THREADS) {
+    const int j = j0 + tid;
+    const int k = kb + j;
+    int a = 0, b = 0, nch = 0;
+    if (j < hc) {
+      a = __ldcg(useg + k);
+      b = __ldcg(useg + k + 1);
+      nch = (b - a + c.C - 1) / c.C;
+    }
+    int tch, tlong;
+    const int och = cta_exscan(nch, tmp, &tch);
+    const int olong = cta_exscan(nch > 1 ? 1 : 0, tmp, &tlong);
+    if (j < hc) {
+      const int off = cb + och;
+      chunk_off[k] = off;
+      for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
+      if (nch > 1) long_u[lb + olong] = k;
+    }
+    cb += tch;
+    lb += tlong;
+  }
+  if (cr == 0 && tid == 0) {
+    chunk_off[U] = NCH;
+    int* cn = c.counts + pn(c, p, n) * CNT_W;
+    cn[CNT_T] = T;
+    cn[CNT_U] = U;
+    cn[CNT_NCH] = NCH;
+    cn[CNT_NLONG] = NLONG;
+  }
+  cluster.sync();  // no CTA exits while a peer may still read its shared memory
+  EMB_TR_END(1, tt);
+  pdl_trigger();
+}
+
+static int cs_ept(int max_tok) {
+  const int per = (max_tok + CL - 1) / CL;
+  const int need = (per + CS_THREADS - 1) / CS_THREADS;
+  const int opts[] = {1, 2, 3, 4, 6, 8};
+  for (int e : opts)
+    if (e >= need) return e;
+  return -1;
+}
+
+size_t sort_smem_bytes(int max_tok, bool key64) {
+  const int e = cs_ept(max_tok);
+  if (e < 0) return (size_t)1 << 30;
+  return (size_t)2 * e * CS_THREADS * (key64 ? 8 : 4);
+}
+
+template <typename K>
+static void* csort_fn(int ept) {
+  switch (ept) {
+    case 1: return (void*)csort_kernel<K, 1>;
+    case 2: return (void*)csort_kernel<K, 2>;
+    case 3: return (void*)csort_kernel<K, 3>;
+    case 4: return (void*)csort_kernel<K, 4>;
+    case 6: return (void*)csort_kernel<K, 6>;
+    case 8: return (void*)csort_kernel<K, 8>;
+    default: return nullptr;
+  }
+}
+
+cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem) {
+  void* f = key64 ? csort_fn<unsigned long long>(cs_ept(max_tok)) : csort_fn<uint32_t>(cs_ept(max_tok));
+  if (!f) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
+                        cudaStream_t s) {
+  void* f = key64 ? csort_fn<unsigned long long>(cs_ept(c.max_tok)) : csort_fn<uint32_t>(cs_ept(c.max_tok));
+  if (!f) return cudaErrorInvalidValue;
+  DevCtx cc = c;
+  void* args[] = {&cc, &p, &own_ids, &own_n};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c.N * CL);
+  cfg.blockDim = dim3(CS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelExC(&cfg, f, args);
+}
+
+}  // namespace emb
