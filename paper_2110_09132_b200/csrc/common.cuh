@@ -81,6 +81,9 @@ struct DevCtx {
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
+  unsigned int* sorted;   // [2]   t of the last completed sort of parity p (gate before the coalesce)
+  unsigned int* sort_cnt; // [2]   clusters of the running sort that finished (re-armed by the last)
+  unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
@@ -140,6 +143,17 @@ __device__ __forceinline__ bool is_prior(const DevCtx& c, int p, uint32_t t, int
   return c.mode != SPLIT || __ldcg(c.nextmark + (size_t)p * c.L + id) == (int)(t + 1);
 }
 
+// Position-hashed id for the N == 1 prefetch check: the sums over a batch of
+// h(id, j) computed by the forward (ids of t) and by the sort (next_ids given
+// at t-1) must agree (a mismatch is missed with probability ~2^-32).
+__device__ __forceinline__ unsigned prefetch_hash(int id, int j) {
+  unsigned x = (unsigned)id * 0x9E3779B1u ^ ((unsigned)j * 0x85EBCA77u + 0x165667B1u);
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  return x;
+}
+
 // ----------------------------------------------------------------- memory model
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -148,6 +162,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -264,6 +264,9 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cfg->mode == EMB_BWD_SPLIT && N > 1) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
     if (cfg->mode == EMB_BWD_RAW) ALLOC(c.gc_owner, 2 * N * T * pl.d * 4);
     ALLOC(c.t_rec, 2 * 4);
+    ALLOC(c.sorted, 2 * 4);
+    ALLOC(c.sort_cnt, 2 * 4);
+    ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
     ALLOC(c.stats, 3 * N * 8);
@@ -376,10 +379,9 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->it += 1;
   const int p = (int)(ctx->it & 1);
   if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
-  if (ctx->mark_pending) {  // N == 1: the prefetch copy ran on the side stream
-    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_marked, 0));
-    ctx->mark_pending = false;
-  }
+  // N == 1: the prefetch copy (mark) runs on the side stream and nothing on
+  // the main stream reads it (the prefetch check is a fingerprint, k_gate.cu)
+  ctx->mark_pending = false;
   const int pre = ctx->prefetched ? 1 : 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, 0, stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
@@ -470,10 +472,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       ctx->sort_pending[p ^ 1] = true;
     }
   }
-  if (ctx->sort_pending[p]) {  // the sort of this batch (aux stream) must be complete
-    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
-    ctx->sort_pending[p] = false;
-  }
+  // the sort of this batch (aux stream) must be complete: a one-warp gate on a
+  // device flag the sort sets (a host event here would break the PDL chain);
+  // at N == 1 it also checks the prefetch fingerprints
+  CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
+  ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
     CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
     CKC(ctx, gate(ctx, p, GATE_PUB0, 0, stream));

@@ -52,10 +52,16 @@ __device__ __forceinline__ void reduce_rows(const char* __restrict__ base, size_
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < V * EPV; ++i) acc[i] = 0.f;
+  static_assert(32 % RB == 0, "row batches must tile the 32-position windows");
+  int mypos = 0;  // lane j holds perm[window + j]: one load per 32 rows, not one per row batch
   for (int i = b; i < e; i += RB) {
+    if (((i - b) & 31) == 0) {
+      const int j = i + lane;
+      mypos = (j < e) ? __ldg(perm + j) : 0;
+    }
     int pos[RB];
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) pos[rr] = (i + rr < e) ? __ldg(perm + i + rr) : 0;
+    for (int rr = 0; rr < RB; ++rr) pos[rr] = __shfl_sync(0xffffffffu, mypos, (i - b + rr) & 31);
     uint4 buf[RB][V];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {

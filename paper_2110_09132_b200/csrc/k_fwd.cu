@@ -52,11 +52,20 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     if (tid < c.N) *ntok_of(c, tid, p, c.r) = n;
     if (tid == 0)
       for (int s = 0; s < c.N; ++s) atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n * 4ull);
-  } else {
+  } else if (c.N > 1) {
     const int* mine = gids_of(c, c.r, p, c.r);  // prefetched by backward(t-1): must be the promised ids
     for (int j = tid; j < n; j += nth)
       if (mine[j] != ids[j]) atomicOr(c.err, ERR_STATE);
     if (tid == 0 && *ntok_of(c, c.r, p, c.r) != n) atomicOr(c.err, ERR_STATE);
+  } else {
+    // N == 1: the sort of this batch read next_ids directly (no copy to order
+    // against): fingerprint the ids; the gate before the coalesce compares
+    unsigned h = 0;
+    for (int j = tid; j < n; j += nth) h += prefetch_hash(__ldg(ids + j), j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0 && h) atomicAdd(&c.fp[p * 4 + 0], h);
+    if (tid == 0) atomicAdd(&c.fp[p * 4 + 1], (unsigned)n);
   }
   // every owner applied the prior part of t-1 and the scheduled part of t-2:
   // the gate before this kernel (N > 1) waited for their flags

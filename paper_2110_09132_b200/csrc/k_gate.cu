@@ -63,6 +63,23 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         EMB_TR_END(10 + kind, t);
         break;
       }
+      case GATE_SORTED: {
+        // coalesce of t: the sort of batch t (aux stream) completed — a local
+        // flag instead of a host event keeps the main stream's PDL chain; at
+        // N == 1 also the prefetch check (fingerprints of fwd(t) and sort(t))
+        const uint32_t t = c.t_rec[p];
+        EMB_TR_BEGIN(10 + kind, t);
+        const unsigned long long t0 = globaltimer();
+        while ((int)(ld_acquire_gpu(c.sorted + p) - t) < 0) {
+          __nanosleep(32);
+          if (globaltimer() - t0 > c.timeout_ns) { atomicOr(c.err, ERR_TIMEOUT); break; }
+        }
+        unsigned* f = c.fp + p * 4;
+        if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
+        f[0] = f[1] = f[2] = f[3] = 0;
+        EMB_TR_END(10 + kind, t);
+        break;
+      }
       default:
         atomicOr(c.err, ERR_STATE);
     }

@@ -112,19 +112,28 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   const long long L = c.L;
 
   // ---- load: key = (id' << posbits) | pos, id' = L for dropped tokens (reading R6)
+  unsigned fph = 0;  // N == 1 prefetch fingerprint (see fwd_kernel)
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const int i = tid + e * CS_THREADS;
     if (i < cnt) {
       const int gi = lo + i;
       const int id = __ldcg(g + gi);
+      fph += prefetch_hash(id, gi);
       long long idp = id;
       if ((unsigned)id >= (unsigned long long)L) idp = L;               // invalid (the forward flags it)
       else if (c.pad_id >= 0 && (long long)id == c.pad_id) idp = L;     // pad: no gradient
       keyA[i] = (K(idp) << posbits) | K(gi);
     }
   }
+  if (own) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fph += __shfl_xor_sync(0xffffffffu, fph, o);
+    if (lane == 0 && fph) atomicAdd(&c.fp[p * 4 + 2], fph);
+    if (cr == 0 && tid == 0) atomicAdd(&c.fp[p * 4 + 3], (unsigned)T);
+  }
   __syncthreads();
+  EMB_TR_AT(1, tt, 4);
 
   // ---- stable LSD radix over the id bits, 8-bit digits, scatter through DSMEM
   const int top = posbits + idbits;
@@ -184,6 +193,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     K* sw = keyA; keyA = keyB; keyB = sw;
   }
 
+  EMB_TR_AT(1, tt, 5);
   // ---- heads -> unique kept ids (ascending), segments, owner routing
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
   int* perm = c.perm + bpn;
@@ -257,6 +267,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   if (cr == 0 && tid == 0) useg[U] = Tk;  // end of the last kept segment (kept keys sort first)
   cluster.sync();  // useg[] of the whole cluster is in global memory (release / acquire at cluster scope)
 
+  EMB_TR_AT(1, tt, 6);
   // ---- reduce chunks of C rows per unique: descriptors, multi-chunk list
   int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
   int4* chunk_desc = c.chunk_desc + pn(c, p, n) * (size_t)c.max_chunks;
@@ -308,7 +319,18 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     cn[CNT_NCH] = NCH;
     cn[CNT_NLONG] = NLONG;
   }
+  EMB_TR_AT(1, tt, 7);
   cluster.sync();  // no CTA exits while a peer may still read its shared memory
+  if (cr == 0 && tid == 0) {
+    // sort of parity p complete once every source's cluster arrived: the gate
+    // before the coalesce waits for sorted[p] (no host event on the main stream)
+    __threadfence();
+    if (atomicAdd(&c.sort_cnt[p], 1u) == (unsigned)c.N - 1) {
+      c.sort_cnt[p] = 0;
+      __threadfence();
+      st_release_gpu(&c.sorted[p], tt);
+    }
+  }
   EMB_TR_END(1, tt);
   pdl_trigger();
 }
