@@ -135,8 +135,8 @@ typedef enum {
   EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src sorted by (dropped, id,
                            position); slot k's rows are perm[seg_start[k] .. seg_end[k]) */
   EMB_DBG_ISSUE_LOG = 4, /* int64 [k]     dense-queue tickets in issue order          */
-  EMB_DBG_TIMESTAMPS = 5  /* uint64 [16][16][4] kernel trace ring: [t%16][kernel kind][entered,
-                             waited, finished] globaltimer ns (EMB_TRACE builds; zeros otherwise) */
+  EMB_DBG_TIMESTAMPS = 5  /* uint64 [16][20][8] kernel trace ring: [t%16][kernel kind][entered,
+                             waited, finished, phase stamps] globaltimer ns (EMB_TRACE builds) */
 } emb_debug_item;
 
 typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1, EMB_STATE_ADAM_V = 2 } emb_state_item;

@@ -83,6 +83,8 @@ struct DevCtx {
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
   unsigned int* sorted;   // [2]   t of the last completed sort of parity p (gate before the coalesce)
   unsigned int* sort_cnt; // [2]   clusters of the running sort that finished (re-armed by the last)
+  unsigned int* marked;   // [2]   t of the last completed mark (prefetch push + D_next tags) of parity p
+  unsigned int* mark_cnt; // [2]   CTAs of the running mark that finished (re-armed by the last)
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
@@ -91,13 +93,14 @@ struct DevCtx {
 };
 
 // Kernel trace (EMB_TRACE builds only; a debug aid, compiled out otherwise):
-// dbg_ts[(t & 15)][kind][8] globaltimer stamps — 0: block 0 entered (before
+// dbg_ts[(t & 15)][EMB_TRACE_KINDS][8] globaltimer stamps — 0: block 0 entered (before
 // the PDL wait), 1: block 0 past its dependency/flag waits, 2: last block
 // finished (max over blocks), 3..7: block 0 at kernel-specific points
 // (EMB_TR_AT).  Read with emb_debug_copy(EMB_DBG_TIMESTAMPS).
-#define EMB_TRACE_SLOTS (16 * 16 * 8)
+#define EMB_TRACE_KINDS 20
+#define EMB_TRACE_SLOTS (16 * EMB_TRACE_KINDS * 8)
 #ifdef EMB_TRACE
-#define EMB_TR_IDX(kind, t, slot) (((((t)&15) * 16) + (kind)) * 8 + (slot))
+#define EMB_TR_IDX(kind, t, slot) (((((t)&15) * EMB_TRACE_KINDS) + (kind)) * 8 + (slot))
 #define EMB_TR_ENTRY() const unsigned long long tr_entry_ = globaltimer()
 #define EMB_TR_BEGIN(kind, t)                                                             \
   do {                                                                                    \

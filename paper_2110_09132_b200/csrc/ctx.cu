@@ -266,6 +266,8 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.t_rec, 2 * 4);
     ALLOC(c.sorted, 2 * 4);
     ALLOC(c.sort_cnt, 2 * 4);
+    ALLOC(c.marked, 2 * 4);
+    ALLOC(c.mark_cnt, 2 * 4);
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
@@ -383,7 +385,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // the main stream reads it (the prefetch check is a fingerprint, k_gate.cu)
   ctx->mark_pending = false;
   const int pre = ctx->prefetched ? 1 : 0;
-  CKC(ctx, gate(ctx, p, GATE_FWD, 0, stream));
+  CKC(ctx, gate(ctx, p, GATE_FWD, pre, stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
@@ -452,11 +454,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     ctx->side_used = true;
     ctx->aux_used = true;
   } else {
-    // a5: prefetch all-gather of the next ids + D_next marks: the owners need
-    // the marks before the coalesce (prior rows travel first): main stream.
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, stream, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, stream); }));
-    CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
+    // a5 on the aux stream: the prefetch push of ids(t+1) and the D_next tags
+    // overlap the segmented reduce (which does not need them); only the apply,
+    // which routes prior vs scheduled rows, waits for them (GATE_MARKED).
     CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, aux); }));
     ctx->aux_used = true;
     // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
     CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
@@ -484,6 +486,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
+    if (mode == EMB_BWD_SPLIT) CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
     CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
-  EMB_TR_BEGIN(15, t);
+  EMB_TR_BEGIN(16, t);
   const int* cnt = counts_of(c, p, r);
   const int U = cnt[CNT_U], NLONG = cnt[CNT_NLONG];
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
         if (ok[j]) apply_store<DT>(c, p, t, kk[j], id[j], c16, g[j], st[j], alpha);
     }
   }
-  EMB_TR_END(15, t);
+  EMB_TR_END(16, t);
   pdl_trigger();
 }
 

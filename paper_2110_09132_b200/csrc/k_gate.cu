@@ -23,6 +23,18 @@
 
 namespace emb {
 
+// spin (bounded) until a local epoch flag reaches t
+__device__ __forceinline__ void wait_local(const DevCtx& c, const uint32_t* flag, uint32_t t) {
+  const unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire_gpu(flag) - t) < 0) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > c.timeout_ns) {
+      atomicOr(c.err, ERR_TIMEOUT);
+      return;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int flag_arg) {
   EMB_TR_ENTRY();
   pdl_wait();
@@ -38,6 +50,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         Flags* f = flags_of(c, c.r);
         wait_all(c, f->prior_done, t - 1);
         wait_all(c, f->def_done, t - 2);
+        if (flag_arg) wait_local(c, c.marked + (p ^ 1), t - 1);  // the prefetch copy this forward checks
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -63,17 +76,21 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         EMB_TR_END(10 + kind, t);
         break;
       }
+      case GATE_MARKED: {
+        // apply of t (SPLIT): the D_next tags of t+1 are complete (mark, aux stream)
+        const uint32_t t = c.t_rec[p];
+        EMB_TR_BEGIN(10 + kind, t);
+        wait_local(c, c.marked + p, t);
+        EMB_TR_END(10 + kind, t);
+        break;
+      }
       case GATE_SORTED: {
         // coalesce of t: the sort of batch t (aux stream) completed — a local
         // flag instead of a host event keeps the main stream's PDL chain; at
         // N == 1 also the prefetch check (fingerprints of fwd(t) and sort(t))
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
-        const unsigned long long t0 = globaltimer();
-        while ((int)(ld_acquire_gpu(c.sorted + p) - t) < 0) {
-          __nanosleep(32);
-          if (globaltimer() - t0 > c.timeout_ns) { atomicOr(c.err, ERR_TIMEOUT); break; }
-        }
+        wait_local(c, c.sorted + p, t);
         unsigned* f = c.fp + p * 4;
         if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
         f[0] = f[1] = f[2] = f[3] = 0;

@@ -136,6 +136,16 @@ __global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* 
       }
     }
   }
+  // completion flag for the main stream's gate (mark runs on the aux stream at N > 1)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&c.mark_cnt[p], 1u) == gridDim.x - 1) {
+      c.mark_cnt[p] = 0;
+      __threadfence();
+      st_release_gpu(&c.marked[p], t);
+    }
+  }
   EMB_TR_END(2, t);
   pdl_trigger();
 }

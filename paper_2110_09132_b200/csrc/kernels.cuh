@@ -53,7 +53,7 @@ inline cudaError_t launch_pdl_raw(const void* f, dim3 grid, dim3 block, size_t s
 
 // Peer-flag gates (k_gate.cu): every N > 1 cross-GPU wait runs in a one-warp
 // kernel right before the consumer; compute kernels never spin.
-enum GateKind { GATE_FWD = 0, GATE_SORT = 1, GATE_PUB0 = 2, GATE_PUB1 = 3, GATE_SORTED = 4 };
+enum GateKind { GATE_FWD = 0, GATE_SORT = 1, GATE_PUB0 = 2, GATE_PUB1 = 3, GATE_SORTED = 4, GATE_MARKED = 5 };
 cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s);
 
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,

@@ -9,9 +9,9 @@ import sys
 import numpy as np
 
 NAMES = ["fwd", "sort", "mark", "coal", "merge0", "defpush", "merge1", "rawpush", "rawcoal", "tables",
-         "gate_fwd", "gate_sort", "gate_pub0", "gate_pub1", "gate_sorted", "apply"]
+         "gate_fwd", "gate_sort", "gate_pub0", "gate_pub1", "gate_sorted", "gate_marked", "apply", "k17", "k18", "k19"]
 files = sys.argv[1:]
-rings = [np.load(f).view(np.uint64).astype(np.int64).reshape(16, 16, 8) for f in files]
+rings = [np.load(f).view(np.uint64).astype(np.int64).reshape(16, 20, 8) for f in files]
 base_rank = rings[0]
 for f, ring in zip(files, rings):
     print(f)
@@ -20,7 +20,7 @@ for f, ring in zip(files, rings):
     its = [i for i in order if ring[i, 0, 0] > 0][2:-1]
     steps = np.diff(sorted(ring[its, 0, 0])) / 1e3
     print(f"  iterations {len(its)}  mean fwd-to-fwd {steps.mean():.1f} us  (min {steps.min():.1f} max {steps.max():.1f})")
-    for k in range(16):
+    for k in range(20):
         rel = []
         for i in its:
             e = ring[i, k]
