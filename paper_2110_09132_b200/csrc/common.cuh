@@ -85,9 +85,12 @@ struct DevCtx {
   unsigned int* sort_cnt; // [2]   clusters of the running sort that finished (re-armed by the last)
   unsigned int* marked;   // [2]   t of the last completed mark (prefetch push + D_next tags) of parity p
   unsigned int* mark_cnt; // [2]   CTAs of the running mark that finished (re-armed by the last)
+  unsigned int* seq;      // [4]   main-stream progress: [SEQ_BWD] = t past gate_sorted, [SEQ_APPLIED] = t past apply
+  unsigned int* seen;     // [4]   per waiting stream: how many of those steps it has consumed
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
+  unsigned* err_info;     // [4] first expired wait: site, observed, target, set
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
   unsigned long long* dbg_ts; // [EMB_TRACE_SLOTS] kernel trace (EMB_TRACE builds only)
 };
@@ -189,13 +192,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Spin until *flag >= target (epoch compare, wrap-safe) or the bound expires.
-__device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag, uint32_t target) {
+// On expiry: sticky ERR_TIMEOUT, and the first expired wait is described in
+// err_info = {site, observed value, target, 1} (emb_debug_copy EMB_DBG_ERRINFO).
+__device__ __forceinline__ void note_timeout(const DevCtx& c, int site, uint32_t seen, uint32_t target) {
+  atomicOr(c.err, ERR_TIMEOUT);
+  if (atomicCAS(c.err_info + 3, 0u, 1u) == 0u) {
+    c.err_info[0] = (unsigned)site;
+    c.err_info[1] = seen;
+    c.err_info[2] = target;
+  }
+}
+__device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag, uint32_t target, int site = 0) {
   if ((int)(ld_acquire_sys(flag) - target) >= 0) return;
   unsigned long long t0 = globaltimer();
-  while ((int)(ld_acquire_sys(flag) - target) < 0) {
+  uint32_t v;
+  while ((int)((v = ld_acquire_sys(flag)) - target) < 0) {
     __nanosleep(32);
     if (globaltimer() - t0 > c.timeout_ns) {
-      atomicOr(c.err, ERR_TIMEOUT);
+      note_timeout(c, site, v, target);
       return;
     }
   }
@@ -203,9 +217,9 @@ __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag,
 
 // N == 1: every producer/consumer pair is ordered by the stream or an event,
 // so the flag protocol (and its system fences) is skipped entirely.
-__device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target) {
+__device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target, int site = 0) {
   if (c.N == 1) return;
-  for (int s = 0; s < c.N; ++s) wait_flag(c, flags + s, target);
+  for (int s = 0; s < c.N; ++s) wait_flag(c, flags + s, target, site * 16 + s);
 }
 
 // Publish value v into slot [c.r] of field `field` (an offset into Flags) of

@@ -268,14 +268,21 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.sort_cnt, 2 * 4);
     ALLOC(c.marked, 2 * 4);
     ALLOC(c.mark_cnt, 2 * 4);
+    ALLOC(c.seq, 4 * 4);
+    ALLOC(c.seen, 4 * 4);
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
+    ALLOC(c.err_info, 16);
     ALLOC(c.stats, 3 * N * 8);
     ALLOC(c.dbg_ts, EMB_TRACE_SLOTS * 8);
   }
 #undef ALLOC
   if (sort_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem) != cudaSuccess) goto fail;
+  // load every kernel now (see kernels.cuh: preload)
+  if (preload_fwd() != cudaSuccess || preload_bwd() != cudaSuccess || preload_route() != cudaSuccess ||
+      preload_sort() != cudaSuccess || preload_gate() != cudaSuccess)
+    goto fail;
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
@@ -330,7 +337,7 @@ __global__ void boot_kernel(DevCtx c, uint32_t val) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
   for (int s = 0; s < c.N; ++s) st_release_sys(&flags_of(c, s)->boot[c.r], val);
-  for (int s = 0; s < c.N; ++s) wait_flag(c, &flags_of(c, c.r)->boot[s], val);
+  for (int s = 0; s < c.N; ++s) wait_flag(c, &flags_of(c, c.r)->boot[s], val, 12 * 16 + s);
 }
 
 emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8_t* nccl_id,
@@ -380,7 +387,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   ctx->it += 1;
   const int p = (int)(ctx->it & 1);
-  if (ctx->def_pending[p]) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_def[p], 0));
+  // (SPLIT, N > 1: the scheduled merge of t-2 is waited on device by GATE_FWD's def_done flags)
   // N == 1: the prefetch copy (mark) runs on the side stream and nothing on
   // the main stream reads it (the prefetch check is a fingerprint, k_gate.cu)
   ctx->mark_pending = false;
@@ -424,7 +431,19 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   cudaStream_t aux = ctx->aux;
   const int N = ctx->pl.N;
   const int do_mark = (mode == EMB_BWD_SPLIT && next_ids) ? 1 : 0;
-  CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));  // caller's next_ids / dY are ready in stream order
+  // Fork (not join): the aux / side streams are ordered after everything the
+  // caller enqueued so far (next_ids / dY ready, forward(t) done).  An event
+  // record on the main stream does not break its programmatic-launch chain; a
+  // wait on the main stream would, so every join back into it is a device
+  // flag gate instead (GATE_SORTED, GATE_MARKED, GATE_FWD's def_done).
+  CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
+  CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
+  CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_main[p], 0));
+  ctx->aux_used = ctx->side_used = true;
+  // finer-grained waits of the side stream on main-stream progress (device flags)
+  auto seq_gate = [&](cudaStream_t s2, int si, int wi) {
+    return run_k(ctx, EMB_K_GATE, s2, [&] { return launch_gate(ctx->dc, p, GATE_SEQ, (si << 8) | wi, s2); });
+  };
   if (N == 1) {
     // N == 1: nothing on the critical path needs the D_next marks (the coalesce
     // applies every row), so
@@ -433,7 +452,6 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     //   side: a5 (ids copy for the forward's prefetch check + D_next marks) and
     //         the a8 slot tables of this batch.
     // next_ids is read asynchronously until the next backward (header contract).
-    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
     if (next_ids) {
       if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_tables[p ^ 1], 0));
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
@@ -443,11 +461,10 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       ctx->sort_pending[p ^ 1] = true;
       ctx->tables_pending[p ^ 1] = false;
     }
-    CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_main[p], 0));
+    CKC(ctx, seq_gate(side, SEQ_BWD, W_SIDE));  // also orders after sort(t) (GATE_SORTED waited it)
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
     ctx->mark_pending = true;
-    if (ctx->sort_pending[p]) CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_sorted[p], 0));
     CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_tables[p], side));
     ctx->tables_pending[p] = true;
@@ -457,15 +474,14 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // a5 on the aux stream: the prefetch push of ids(t+1) and the D_next tags
     // overlap the segmented reduce (which does not need them); only the apply,
     // which routes prior vs scheduled rows, waits for them (GATE_MARKED).
-    CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, aux); }));
     ctx->aux_used = true;
     // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
     CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
     if (next_ids) {
       // a6 for the next batch, one iteration ahead.  Its parity's previous user
-      // (the scheduled merge of t-1) must be done with the routing tables.
-      if (ctx->def_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_def[p ^ 1], 0));
+      // (the scheduled merge of t-1) must be done with the routing tables: the
+      // gate waits this rank's def_done flag.
       CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 0, aux));
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
         return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
@@ -495,15 +511,14 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
     }
     if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) {
-      // scheduled part: lowest-priority side stream, after the prior part
-      CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));
-      CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));
+      // scheduled part: lowest-priority side stream, once the apply of t staged
+      // the scheduled rows (sequence flag set by GATE_PUB0)
+      CKC(ctx, seq_gate(side, SEQ_APPLIED, W_SIDE));
       if (ctx->pl.N > 1)  // N == 1: coal wrote every row to its receive slot directly
         CKC(ctx, run_k(ctx, EMB_K_DEFPUSH, side, [&] { return launch_defpush(c, lc, p, side); }));
       CKC(ctx, gate(ctx, p, GATE_PUB1, 0, side));
       CKC(ctx, run_k(ctx, EMB_K_MERGE1, side, [&] { return launch_merge(c, lc, p, 1, side); }));
-      CKC(ctx, cudaEventRecord(ctx->ev_def[p], ctx->side));
-      ctx->def_pending[p] = true;
+      CKC(ctx, gate(ctx, p, GATE_DEFDONE, 0, side));  // def_done(t) to every owner
       ctx->side_used = true;
     }
   }
@@ -674,6 +689,12 @@ emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, s
   *n = 0;
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
   CKC(ctx, cudaDeviceSynchronize());
+  if (item == EMB_DBG_ERRINFO) {
+    *n = 4;
+    if (cap < 16) return EMB_ERR_CAPACITY;
+    CKC(ctx, cudaMemcpy(host, ctx->dc.err_info, 16, cudaMemcpyDeviceToHost));
+    return EMB_OK;
+  }
   if (item == EMB_DBG_TIMESTAMPS) {
     *n = EMB_TRACE_SLOTS;
     if (cap < EMB_TRACE_SLOTS * 8) return EMB_ERR_CAPACITY;

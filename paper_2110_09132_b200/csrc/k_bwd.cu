@@ -800,4 +800,26 @@ cudaError_t launch_merge(const DevCtx& c, const LaunchCfg& L, int p, int part, c
              : launch_pdl(merge_kernel<F32, false>, g, b, 0, s, c, p, part, G);
 }
 
+template <int DT>
+static cudaError_t preload_dt() {
+  const void* fs[] = {(const void*)coal_reduce_kernel<DT, 1>, (const void*)coal_reduce_kernel<DT, 2>,
+                      (const void*)coal_reduce_kernel<DT, 4>, (const void*)coal_reduce_kernel<DT, 8>,
+                      (const void*)rawcoal_a_kernel<DT, 1>,   (const void*)rawcoal_a_kernel<DT, 2>,
+                      (const void*)rawcoal_a_kernel<DT, 4>,   (const void*)rawcoal_a_kernel<DT, 8>,
+                      (const void*)rawcoal_b_kernel<DT, 1>,   (const void*)rawcoal_b_kernel<DT, 2>,
+                      (const void*)rawcoal_b_kernel<DT, 4>,   (const void*)rawcoal_b_kernel<DT, 8>,
+                      (const void*)coal_apply_kernel<DT>,     (const void*)merge_kernel<DT, true>,
+                      (const void*)merge_kernel<DT, false>};
+  for (const void* f : fs)
+    if (cudaError_t e = preload(f)) return e;
+  return cudaSuccess;
+}
+
+cudaError_t preload_bwd() {
+  if (cudaError_t e = preload_dt<F32>()) return e;
+  if (cudaError_t e = preload_dt<BF16>()) return e;
+  if (cudaError_t e = preload((const void*)defpush_kernel)) return e;
+  return preload((const void*)rawpush_kernel);
+}
+
 }  // namespace emb

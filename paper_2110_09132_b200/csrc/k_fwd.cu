@@ -130,4 +130,11 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t preload_fwd() {
+  for (const void* f : {(const void*)fwd_kernel<1>, (const void*)fwd_kernel<2>, (const void*)fwd_kernel<4>,
+                        (const void*)fwd_kernel<8>})
+    if (cudaError_t e = preload(f)) return e;
+  return cudaSuccess;
+}
+
 }  // namespace emb

@@ -24,12 +24,13 @@
 namespace emb {
 
 // spin (bounded) until a local epoch flag reaches t
-__device__ __forceinline__ void wait_local(const DevCtx& c, const uint32_t* flag, uint32_t t) {
+__device__ __forceinline__ void wait_local(const DevCtx& c, const uint32_t* flag, uint32_t t, int site) {
   const unsigned long long t0 = globaltimer();
-  while ((int)(ld_acquire_gpu(flag) - t) < 0) {
+  uint32_t v;
+  while ((int)((v = ld_acquire_gpu(flag)) - t) < 0) {
     __nanosleep(32);
     if (globaltimer() - t0 > c.timeout_ns) {
-      atomicOr(c.err, ERR_TIMEOUT);
+      note_timeout(c, site, v, t);
       return;
     }
   }
@@ -41,16 +42,17 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
   if (threadIdx.x == 0) {
     switch (kind) {
       case GATE_FWD: {
-        // forward(t): the main stream completed merge(prior, t-1) and (host event)
-        // merge(scheduled, t-2); every owner must have done the same
+        // forward(t): the main stream completed merge(prior, t-1): publish it;
+        // SPLIT: def_done(t-2) comes from GATE_DEFDONE on the side stream.  Every
+        // owner (this rank included) must have applied both parts.
         const uint32_t t = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, t);
-        const uint32_t dd = (c.mode == SPLIT) ? t - 2 : t - 1;
-        publish2(c, EMB_FLAG_OFF(prior_done), t - 1, t >= 2, EMB_FLAG_OFF(def_done), dd, (int)dd >= 1);
+        publish2(c, EMB_FLAG_OFF(prior_done), t - 1, t >= 2, EMB_FLAG_OFF(def_done), t - 1,
+                 c.mode != SPLIT && t >= 2);
         Flags* f = flags_of(c, c.r);
-        wait_all(c, f->prior_done, t - 1);
-        wait_all(c, f->def_done, t - 2);
-        if (flag_arg) wait_local(c, c.marked + (p ^ 1), t - 1);  // the prefetch copy this forward checks
+        wait_all(c, f->prior_done, t - 1, 1);
+        wait_all(c, f->def_done, t - 2, 2);
+        if (flag_arg) wait_local(c, c.marked + (p ^ 1), t - 1, 3);  // the prefetch copy this forward checks
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -60,7 +62,10 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         const uint32_t tt = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, tt);
         if (flag_arg) publish(c, EMB_FLAG_OFF(ids), tt);
-        wait_all(c, flags_of(c, c.r)->ids, tt);
+        wait_all(c, flags_of(c, c.r)->ids, tt, 4);
+        // the routing tables of parity p are free once this rank's scheduled merge
+        // of tt-2 (side stream) is done
+        if (c.mode == SPLIT && tt >= 3) wait_flag(c, &flags_of(c, c.r)->def_done[c.r], tt - 2, 5 * 16);
         EMB_TR_END(10 + kind, tt);
         break;
       }
@@ -71,8 +76,9 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
         const int part = (kind == GATE_PUB1) ? 1 : 0;
+        if (!part) st_release_gpu(c.seq + SEQ_APPLIED, t);  // the apply of t completed (side stream waits)
         publish(c, part ? EMB_FLAG_OFF(pub[1]) : EMB_FLAG_OFF(pub[0]), t);
-        wait_all(c, flags_of(c, c.r)->pub[part], t);
+        wait_all(c, flags_of(c, c.r)->pub[part], t, 6 + part);
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // apply of t (SPLIT): the D_next tags of t+1 are complete (mark, aux stream)
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
-        wait_local(c, c.marked + p, t);
+        wait_local(c, c.marked + p, t, 8 * 16);
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -90,11 +96,33 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // N == 1 also the prefetch check (fingerprints of fwd(t) and sort(t))
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
-        wait_local(c, c.sorted + p, t);
+        wait_local(c, c.sorted + p, t, 9 * 16);
         unsigned* f = c.fp + p * 4;
         if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
         f[0] = f[1] = f[2] = f[3] = 0;
+        // forward(t) and sort(t) done, next_ids of backward(t) ready in stream
+        // order: the aux / side streams may start backward(t)'s work
+        st_release_gpu(c.seq + SEQ_BWD, t);
         EMB_TR_END(10 + kind, t);
+        break;
+      }
+      case GATE_DEFDONE: {
+        // the scheduled merge of t (this stream's predecessor) completed
+        const uint32_t t = c.t_rec[p];
+        EMB_TR_BEGIN(10 + kind, t);
+        publish(c, EMB_FLAG_OFF(def_done), t);
+        EMB_TR_END(10 + kind, t);
+        break;
+      }
+      case GATE_SEQ: {
+        // the next main-stream step of kind `si` (host events would break the
+        // main stream's programmatic-launch chain)
+        const int si = flag_arg >> 8, wi = flag_arg & 255;
+        const uint32_t target = c.seen[wi] + 1;
+        EMB_TR_BEGIN(18, target);
+        wait_local(c, c.seq + si, target, 10 * 16 + si * 4 + wi);
+        c.seen[wi] = target;
+        EMB_TR_END(18, target);
         break;
       }
       default:
@@ -108,5 +136,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
 cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s) {
   return launch_pdl(gate_kernel, dim3(1), dim3(32), 0, s, c, p, kind, flag_arg);
 }
+
+cudaError_t preload_gate() { return preload((const void*)gate_kernel); }
 
 }  // namespace emb

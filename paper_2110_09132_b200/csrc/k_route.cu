@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* 
   }
   EMB_TR_MID(2, t);
   if (do_mark && next_ids != nullptr) {
-    if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1);  // grid = N CTAs: co-resident
+    if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1, 11);  // grid = N CTAs: co-resident
     __syncthreads();
     EMB_TR_WAITED(2, t);
     int* mark = c.nextmark + (size_t)p * c.L;
@@ -238,6 +238,14 @@ cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
   DevCtx cc = c;
   void* args[] = {&cc, &p};
   return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), 0, s, args);
+}
+
+cudaError_t preload_route() {
+  for (const void* f : {(const void*)mark_kernel, (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
+                        (const void*)tables_kernel<4>, (const void*)tables_kernel<5>, (const void*)tables_kernel<8>,
+                        (const void*)tables_kernel<12>, (const void*)tables_kernel<16>})
+    if (cudaError_t e = preload(f)) return e;
+  return cudaSuccess;
 }
 
 }  // namespace emb

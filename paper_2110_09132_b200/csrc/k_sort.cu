@@ -393,4 +393,12 @@ cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, b
   return cudaLaunchKernelExC(&cfg, f, args);
 }
 
+cudaError_t preload_sort() {
+  for (int e : {1, 2, 3, 4, 6, 8}) {
+    if (cudaError_t r = preload(csort_fn<uint32_t>(e))) return r;
+    if (cudaError_t r = preload(csort_fn<unsigned long long>(e))) return r;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace emb

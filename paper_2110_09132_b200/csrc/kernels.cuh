@@ -51,9 +51,34 @@ inline cudaError_t launch_pdl_raw(const void* f, dim3 grid, dim3 block, size_t s
 // so no prefix over the split sits on the critical path.  The slot-ordered
 // Alg. 1 tables (P_n, D_n) are produced off the critical path (tables).
 
+// Lazy module loading (CUDA 12 default) loads a kernel at its first launch and
+// may synchronise the device to do so.  With one-warp gates spinning on flags
+// that a not-yet-launched kernel sets, that synchronisation deadlocks until the
+// wait bound expires; so every kernel is loaded up front (emb_create).
+inline cudaError_t preload(const void* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, f);
+}
+cudaError_t preload_fwd();
+cudaError_t preload_bwd();
+cudaError_t preload_route();
+cudaError_t preload_sort();
+cudaError_t preload_gate();
+
 // Peer-flag gates (k_gate.cu): every N > 1 cross-GPU wait runs in a one-warp
 // kernel right before the consumer; compute kernels never spin.
-enum GateKind { GATE_FWD = 0, GATE_SORT = 1, GATE_PUB0 = 2, GATE_PUB1 = 3, GATE_SORTED = 4, GATE_MARKED = 5 };
+enum GateKind {
+  GATE_FWD = 0,      // main, before forward(t): prior/def parts of every owner applied
+  GATE_SORT = 1,     // aux, before sort(t): every source's ids arrived (+ own merge1(t-2) done)
+  GATE_PUB0 = 2,     // before merge(part 0) / rawcoal: every sender's rows arrived
+  GATE_PUB1 = 3,     // side, before merge(part 1)
+  GATE_SORTED = 4,   // main, before the coalesce: sort(t) done (+ N == 1 prefetch check)
+  GATE_MARKED = 5,   // main, before the apply (SPLIT): D_next tags of t+1 done
+  GATE_DEFDONE = 6,  // side, after merge(part 1): publish def_done(t) to every owner
+  GATE_SEQ = 7       // aux / side: wait for the next main-stream step (flag_arg = seq << 8 | waiter)
+};
+enum SeqIndex { SEQ_BWD = 0, SEQ_APPLIED = 1 };
+enum SeqWaiter { W_AUX = 0, W_SIDE = 1 };
 cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s);
 
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,

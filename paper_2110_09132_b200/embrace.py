@@ -24,7 +24,8 @@ STATUS = {0: "EMB_OK", 1: "EMB_ERR_INVALID_ARG", 2: "EMB_ERR_SHAPE", 3: "EMB_ERR
 EMB_FP32, EMB_BF16 = 0, 1
 EMB_SGD, EMB_ADAM = 0, 1
 EMB_BWD_RAW, EMB_BWD_COAL, EMB_BWD_SPLIT = 0, 1, 2
-EMB_DBG_GIDS, EMB_DBG_SLOT_IDS, EMB_DBG_COUNTS, EMB_DBG_PERM, EMB_DBG_ISSUE_LOG, EMB_DBG_TIMESTAMPS = range(6)
+EMB_DBG_GIDS, EMB_DBG_SLOT_IDS, EMB_DBG_COUNTS, EMB_DBG_PERM, EMB_DBG_ISSUE_LOG, EMB_DBG_TIMESTAMPS, \
+    EMB_DBG_ERRINFO = range(7)
 EMB_STATE_SHARD, EMB_STATE_ADAM_M, EMB_STATE_ADAM_V = range(3)
 MODES = {"raw": EMB_BWD_RAW, "coal": EMB_BWD_COAL, "split": EMB_BWD_SPLIT}
 
