@@ -215,6 +215,19 @@ __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag,
   }
 }
 
+// spin (bounded) until a local epoch flag reaches t
+__device__ __forceinline__ void wait_local(const DevCtx& c, const uint32_t* flag, uint32_t t, int site) {
+  const unsigned long long t0 = globaltimer();
+  uint32_t v;
+  while ((int)((v = ld_acquire_gpu(flag)) - t) < 0) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > c.timeout_ns) {
+      note_timeout(c, site, v, t);
+      return;
+    }
+  }
+}
+
 // N == 1: every producer/consumer pair is ordered by the stream or an event,
 // so the flag protocol (and its system fences) is skipped entirely.
 __device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags, uint32_t target, int site = 0) {

@@ -119,6 +119,7 @@ struct emb_ctx {
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
+  bool fwd_sort_gated = false;  // the last forward's CTA 0 waited for sort(t) (no GATE_SORTED needed)
   bool fwd_pushed = false;   // last forward pushed its ids (route publishes them)
   int last_n = 0;
   DenseQueue* dq = nullptr;
@@ -393,13 +394,19 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->mark_pending = false;
   const int pre = ctx->prefetched ? 1 : 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre, stream));
-  CKC(ctx, run_k(ctx, EMB_K_FWD, stream, [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, stream); }));
+  // sort_gate = 1 would let the forward's CTA 0 wait for sort(t) instead of a
+  // gate kernel before the coalesce; measured slower at N == 1 (the fork of
+  // sort(t+1) then also waits for sort(t)), so the gate kernel stays.
+  const int sort_gate = 0;
+  CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
+                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, stream); }));
+  ctx->fwd_sort_gated = sort_gate != 0;
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
     CKC(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_main[p], 0));
-    CKC(ctx, gate(ctx, p, GATE_SORT, 1, ctx->aux));
+    CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, ctx->aux));
     CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux, [&] {
       return launch_sort(ctx->dc, p, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
     }));
@@ -462,7 +469,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       ctx->tables_pending[p ^ 1] = false;
     }
     CKC(ctx, seq_gate(side, SEQ_BWD, W_SIDE));  // also orders after sort(t) (GATE_SORTED waited it)
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_markpush(c, p, next_ids, n_next, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
     ctx->mark_pending = true;
     CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, side); }));
@@ -474,7 +482,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // a5 on the aux stream: the prefetch push of ids(t+1) and the D_next tags
     // overlap the segmented reduce (which does not need them); only the apply,
     // which routes prior vs scheduled rows, waits for them (GATE_MARKED).
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_mark(c, lc, p, next_ids, n_next, do_mark, aux); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, aux); }));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2, aux));  // publish + wait ids(t+1)
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, aux); }));
     ctx->aux_used = true;
     // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
     CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
@@ -482,7 +492,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       // a6 for the next batch, one iteration ahead.  Its parity's previous user
       // (the scheduled merge of t-1) must be done with the routing tables: the
       // gate waits this rank's def_done flag.
-      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 0, aux));
+      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 4, aux));
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
         return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
       }));
@@ -493,7 +503,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // the sort of this batch (aux stream) must be complete: a one-warp gate on a
   // device flag the sort sets (a host event here would break the PDL chain);
   // at N == 1 it also checks the prefetch fingerprints
-  CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
+  if (!ctx->fwd_sort_gated)
+    CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
   ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
     CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
@@ -501,8 +512,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_RAWCOAL, stream, [&] { return launch_rawcoal(c, lc, p, stream); }));
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
-    CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, stream); }));
-    if (mode == EMB_BWD_SPLIT) CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
+    const int cg = (N == 1 ? 1 : 0) | (mode == EMB_BWD_SPLIT && N > 1 ? 2 : 0);
+    CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, cg, stream); }));
     CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.

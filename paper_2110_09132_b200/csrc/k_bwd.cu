@@ -285,7 +285,8 @@ __device__ __forceinline__ void emit_rows(const DevCtx& c, int p, const float* r
 //               owner's receive row i over NVLink (prior) or the stage
 //               (scheduled).  Every load of an item is issued before its math.
 template <int DT, int V>
-__global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, const char* __restrict__ dY, int p) {
+__global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, const char* __restrict__ dY, int p,
+                                                                  int gate_flags) {
   EMB_TR_ENTRY();
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
@@ -305,6 +306,17 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
     float acc[V * EPV];
     reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, dsc.y, dsc.z, acc);
     store_partial<EPV, V>((dsc.w > 1) ? part + (size_t)ch * c.D : c.gcoal + (size_t)dsc.x * c.D, c.cpr, acc);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // gate duties folded into this kernel's CTA 0 (no gate kernel before the
+    // apply): bit 0, N == 1 prefetch check (fingerprints of fwd(t) and sort(t));
+    // bit 1, SPLIT N > 1: the D_next tags of t+1 (marktag, aux) are complete
+    if (gate_flags & 1) {
+      unsigned* f = c.fp + p * 4;
+      if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
+      f[0] = f[1] = f[2] = f[3] = 0;
+    }
+    if (gate_flags & 2) wait_local(c, c.marked + p, t, 8 * 16 + 1);
   }
   EMB_TR_END(3, t);
   pdl_trigger();
@@ -726,10 +738,11 @@ static int grid_for_warps(long long warps, int cap) {
                : cudaErrorInvalidValue)
 
 template <int DT>
-static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, cudaStream_t s) {
+static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, int gate_flags,
+                                 cudaStream_t s) {
   const int V = (c.cpr + 31) / 32;
   const int ga = grid_for_warps(c.max_chunks, L.nsm * 12);
-  return EMB_LAUNCH_V(V, coal_reduce_kernel, DT, ga, 0, c, y, p);
+  return EMB_LAUNCH_V(V, coal_reduce_kernel, DT, ga, 0, c, y, p, gate_flags);
 }
 
 template <int DT>
@@ -746,9 +759,9 @@ cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaSt
   return c.dtype == BF16 ? apply_dispatch<BF16>(c, L, p, s) : apply_dispatch<F32>(c, L, p, s);
 }
 
-cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s) {
+cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, int gate_flags, cudaStream_t s) {
   const char* y = static_cast<const char*>(dY);
-  return c.dtype == BF16 ? coal_dispatch<BF16>(c, L, y, p, s) : coal_dispatch<F32>(c, L, y, p, s);
+  return c.dtype == BF16 ? coal_dispatch<BF16>(c, L, y, p, gate_flags, s) : coal_dispatch<F32>(c, L, y, p, gate_flags, s);
 }
 
 cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {

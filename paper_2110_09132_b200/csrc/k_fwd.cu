@@ -25,7 +25,8 @@ static constexpr int FWD_ROWS = 4;  // rows in flight per warp
 
 template <int V>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* __restrict__ ids, int n,
-                                                          char* __restrict__ out, int p, int prefetched) {
+                                                          char* __restrict__ out, int p, int prefetched,
+                                                          int sort_gate) {
   EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
@@ -110,12 +111,20 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       }
     }
   }
+  if (sort_gate && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the coalesce that follows needs sort(t) (aux stream, launched one
+    // iteration ahead): CTA 0 waits for it here instead of a gate kernel
+    // between the two (one kernel boundary less on the main stream), then
+    // lets the side stream start this iteration's backward work
+    wait_local(c, c.sorted + p, t, 9 * 16 + 1);
+    st_release_gpu(c.seq + SEQ_BWD, t);
+  }
   EMB_TR_END(0, t);
   pdl_trigger();
 }
 
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, cudaStream_t s) {
+                       int prefetched, int sort_gate, cudaStream_t s) {
   const int warps = (n + FWD_ROWS - 1) / FWD_ROWS;
   int grid = (warps + FWD_THREADS / 32 - 1) / (FWD_THREADS / 32);
   if (grid < 1) grid = 1;
@@ -123,10 +132,10 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   const int V = (c.cpr + 31) / 32;
   char* o = static_cast<char*>(out);
   const dim3 g(grid), b(FWD_THREADS);
-  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched);
-  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched);
-  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched);
-  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched);
+  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
+  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
+  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
+  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
   return cudaErrorInvalidValue;
 }
 

@@ -23,19 +23,6 @@
 
 namespace emb {
 
-// spin (bounded) until a local epoch flag reaches t
-__device__ __forceinline__ void wait_local(const DevCtx& c, const uint32_t* flag, uint32_t t, int site) {
-  const unsigned long long t0 = globaltimer();
-  uint32_t v;
-  while ((int)((v = ld_acquire_gpu(flag)) - t) < 0) {
-    __nanosleep(32);
-    if (globaltimer() - t0 > c.timeout_ns) {
-      note_timeout(c, site, v, t);
-      return;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int flag_arg) {
   EMB_TR_ENTRY();
   pdl_wait();
@@ -57,15 +44,16 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         break;
       }
       case GATE_SORT: {
-        // sort of batch tt: every source's ids must be here.  flag_arg = 1: the
-        // forward (this stream's event predecessor) pushed this rank's ids.
+        // ids of batch tt (parity p).  flag_arg bits: 1 = the predecessor (the
+        // forward or markpush) pushed this rank's ids: publish them; 2 = wait
+        // for every source's ids; 4 (SPLIT) = the routing tables of parity p are
+        // free once this rank's scheduled merge of tt-2 (side stream) is done.
         const uint32_t tt = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, tt);
-        if (flag_arg) publish(c, EMB_FLAG_OFF(ids), tt);
-        wait_all(c, flags_of(c, c.r)->ids, tt, 4);
-        // the routing tables of parity p are free once this rank's scheduled merge
-        // of tt-2 (side stream) is done
-        if (c.mode == SPLIT && tt >= 3) wait_flag(c, &flags_of(c, c.r)->def_done[c.r], tt - 2, 5 * 16);
+        if (flag_arg & 1) publish(c, EMB_FLAG_OFF(ids), tt);
+        if (flag_arg & 2) wait_all(c, flags_of(c, c.r)->ids, tt, 4);
+        if ((flag_arg & 4) && c.mode == SPLIT && tt >= 3)
+          wait_flag(c, &flags_of(c, c.r)->def_done[c.r], tt - 2, 5 * 16);
         EMB_TR_END(10 + kind, tt);
         break;
       }

@@ -9,11 +9,12 @@
 //                                       iteration in memory"
 //
 // B200 design:
-//   mark_kernel(t)   CTA n pushes this rank's next ids to peer n (the prefetch
-//                    all-gather) and, in SPLIT, marks D_next:
-//                    nextmark[p][id] = t+1 (epoch tag, never cleared).  The
-//                    split is then a per-id test in every backward kernel — no
-//                    prefix over the split on the critical path.
+//   markpush(t)      pushes this rank's next ids to every peer (the prefetch
+//                    all-gather); the following gate publishes them
+//   marktag(t)       in SPLIT, marks D_next: nextmark[p][id] = t+1 (epoch tag,
+//                    never cleared).  The split is then a per-id test in every
+//                    backward kernel — no prefix over the split on the
+//                    critical path.
 //   tables_kernel(t) off the critical path: the Alg. 1 split in the paper's
 //                    presentation — slot k = prior ids ascending, then
 //                    scheduled ids ascending (P_n ++ D_n) and p_n — for the
@@ -73,72 +74,75 @@ __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {
   __syncthreads();
 }
 
-// ============================================================== mark (main stream)
-// CTA s pushes this rank's next ids to peer s (prefetch all-gather; the flag is
-// released by that CTA after its own stores), then with do_mark (SPLIT) all
-// CTAs wait for every rank's next ids and tag D_next: nextmark[p][id] = t+1.
-__global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* __restrict__ next_ids, int n_next,
-                                                    int do_mark) {
+// ============================================================== mark (a5)
+// markpush: CTA (s, k) stores slice k of this rank's next ids into peer s's
+// gids[p^1][r] (the prefetch all-gather).  No flag and no fence here: the gate
+// that follows on the stream publishes ids(t+1) after this grid completed.
+static constexpr int MP_SLICES = 4;   // CTAs per destination
+static constexpr int MP_THREADS = 256;
+static constexpr int MK = 8;          // ids in flight per thread
+__global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, const int* __restrict__ next_ids,
+                                                             int n_next) {
   EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p];
+  (void)t;
   EMB_TR_BEGIN(2, t);
-  const int p1 = p ^ 1;
-  const int tid = threadIdx.x;
-  constexpr int MK = 16;  // ids per thread in flight: max_tok <= 16 * 1024
-  if (next_ids != nullptr) {
+  const int s = blockIdx.x % c.N, k = blockIdx.x / c.N;
+  int* dst = gids_of(c, s, p ^ 1, c.r);
+  const int stride = MP_SLICES * MP_THREADS;
+  for (int j0 = k * MP_THREADS + threadIdx.x; j0 < n_next; j0 += MK * stride) {
     int v[MK];
 #pragma unroll
-    for (int k = 0; k < MK; ++k) {
-      const int j = tid + k * 1024;
-      v[k] = (j < n_next) ? __ldg(next_ids + j) : 0;
+    for (int q = 0; q < MK; ++q) {
+      const int j = j0 + q * stride;
+      v[q] = (j < n_next) ? __ldg(next_ids + j) : 0;
     }
-    for (int s = blockIdx.x; s < c.N; s += gridDim.x) {
-      int* dst = gids_of(c, s, p1, c.r);
 #pragma unroll
-      for (int k = 0; k < MK; ++k) {
-        const int j = tid + k * 1024;
-        if (j < n_next) dst[j] = v[k];
-      }
-      if (tid == 0) {
-        *ntok_of(c, s, p1, c.r) = n_next;
-        atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n_next * 4ull);
-      }
-      __syncthreads();
-      EMB_TR_AT(2, t, 4);
-      if (tid == 0 && c.N > 1) {
-        fence_acq_rel_sys();  // cumulative over the CTA's stores (ordered by the barrier)
-        EMB_TR_AT(2, t, 5);
-        st_relaxed_sys(&flags_of(c, s)->ids[c.r], t + 1);
-      }
+    for (int q = 0; q < MK; ++q) {
+      const int j = j0 + q * stride;
+      if (j < n_next) dst[j] = v[q];
     }
   }
-  EMB_TR_MID(2, t);
-  if (do_mark && next_ids != nullptr) {
-    if (tid == 0) wait_all(c, flags_of(c, c.r)->ids, t + 1, 11);  // grid = N CTAs: co-resident
-    __syncthreads();
-    EMB_TR_WAITED(2, t);
+  if (k == 0 && threadIdx.x == 0) {
+    *ntok_of(c, s, p ^ 1, c.r) = n_next;
+    atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n_next * 4ull);
+  }
+  EMB_TR_END(2, t);
+  pdl_trigger();
+}
+
+// marktag: with every rank's next ids here (N > 1: the gate before waited the
+// ids flags), tag D_next: nextmark[p][id] = t+1 (epoch tag, never cleared), so
+// the split is a per-id test everywhere.  Then the completion flag marked[p].
+static constexpr int MT_CTAS_PER_SRC = 8;
+__global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark) {
+  EMB_TR_ENTRY();
+  pdl_wait();
+  const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(17, t);
+  if (do_mark) {
     int* mark = c.nextmark + (size_t)p * c.L;
-    const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
+    const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
     for (int s = 0; s < c.N; ++s) {
-      const int cn = __ldcg(ntok_of(c, c.r, p1, s));
-      const int* gn = gids_of(c, c.r, p1, s);
+      const int cn = __ldcg(ntok_of(c, c.r, p ^ 1, s));
+      const int* gn = gids_of(c, c.r, p ^ 1, s);
       for (int j0 = gtid; j0 < cn; j0 += MK * nthr) {
         int id[MK];
 #pragma unroll
-        for (int k = 0; k < MK; ++k) {
-          const int j = j0 + k * nthr;
-          id[k] = (j < cn) ? __ldcg(gn + j) : -1;
+        for (int q = 0; q < MK; ++q) {
+          const int j = j0 + q * nthr;
+          id[q] = (j < cn) ? __ldcg(gn + j) : -1;
         }
 #pragma unroll
-        for (int k = 0; k < MK; ++k)
-          if ((unsigned)id[k] < (unsigned long long)c.L) mark[id[k]] = (int)(t + 1);
+        for (int q = 0; q < MK; ++q)
+          if ((unsigned)id[q] < (unsigned long long)c.L) mark[id[q]] = (int)(t + 1);
       }
     }
   }
-  // completion flag for the main stream's gate (mark runs on the aux stream at N > 1)
+  // completion flag for the gates of the main stream (the apply, the next forward)
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&c.mark_cnt[p], 1u) == gridDim.x - 1) {
       c.mark_cnt[p] = 0;
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(1024) mark_kernel(DevCtx c, int p, const int* 
       st_release_gpu(&c.marked[p], t);
     }
   }
-  EMB_TR_END(2, t);
+  EMB_TR_END(17, t);
   pdl_trigger();
 }
 
@@ -226,10 +230,12 @@ static void* tables_fn(int ept) {
   return nullptr;
 }
 
-cudaError_t launch_mark(const DevCtx& c, const LaunchCfg& L, int p, const int* next_ids, int n_next, int do_mark,
-                        cudaStream_t s) {
-  (void)L;
-  return launch_pdl(mark_kernel, dim3(c.N), dim3(1024), 0, s, c, p, next_ids, n_next, do_mark);
+cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, cudaStream_t s) {
+  return launch_pdl(markpush_kernel, dim3(c.N * MP_SLICES), dim3(MP_THREADS), 0, s, c, p, next_ids, n_next);
+}
+
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, cudaStream_t s) {
+  return launch_pdl(marktag_kernel, dim3(c.N * MT_CTAS_PER_SRC), dim3(MP_THREADS), 0, s, c, p, do_mark);
 }
 
 cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
@@ -241,7 +247,7 @@ cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
 }
 
 cudaError_t preload_route() {
-  for (const void* f : {(const void*)mark_kernel, (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
+  for (const void* f : {(const void*)markpush_kernel, (const void*)marktag_kernel, (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
                         (const void*)tables_kernel<4>, (const void*)tables_kernel<5>, (const void*)tables_kernel<8>,
                         (const void*)tables_kernel<12>, (const void*)tables_kernel<16>})
     if (cudaError_t e = preload(f)) return e;

@@ -84,23 +84,24 @@ cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStre
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
 // id push or prefetch check, wait for every owner, pull-gather)
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, cudaStream_t s);
+                       int prefetched, int sort_gate, cudaStream_t s);
 // a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
 // owner routing (slotmap) — auxiliary stream, one iteration ahead
 cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
                         cudaStream_t s);
 size_t sort_smem_bytes(int max_tok, bool key64);
 cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
-// a5: prefetch all-gather of the next ids + D_next epoch marks (Alg. 1 line 4's set)
-cudaError_t launch_mark(const DevCtx& c, const LaunchCfg& L, int p, const int* next_ids, int n_next, int do_mark,
-                        cudaStream_t s);
+// a5: prefetch all-gather of the next ids (markpush) and the D_next epoch tags
+// (marktag, + completion flag marked[p]) — Alg. 1 line 4's set
+cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, cudaStream_t s);
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, cudaStream_t s);
 // a8 presentation: Alg. 1 slot tables P_n ++ D_n, counts p_n (stats / debug; off the critical path)
 cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s);
 // a7 + a9 (+a10 for the prior part): sender coalesce — segmented reduce in
 // fp32, long (Zipf-head) segments combined by the last-arriving CTA; N == 1
 // applies the optimizer directly, N > 1 pushes prior rows to the owners and
 // stages scheduled rows.
-cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s);
+cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, int gate_flags, cudaStream_t s);
 // a7 (multi-chunk combine) + a9/a10 or the N == 1 update: coalesced rows -> owners / stage / shard
 cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
 // a12: push the staged scheduled rows to their owners (N > 1)
