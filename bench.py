@@ -39,7 +39,7 @@ METRIC = "sparse embedding fwd+bwd exchange tokens/s at 1/2/4/8 B200; % HBM/NVLi
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="lstm_lm")
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
@@ -124,6 +124,17 @@ def n_batches(cfg, N):
     nb = int(np.ceil(2 * L2_BYTES / per))
     nb += nb % 2                                     # even: graph replays keep the parity
     return max(4, min(nb, 64))
+
+
+def traffic_for(config, world, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest committed
+    ncu --set full capture (profiles/*traffic.json), or None if not captured."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1])).get(f"{config}/n{world}", {})
+    return d.get(kernel)
 
 
 def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
@@ -410,7 +421,7 @@ def main():
             "achieved": round(hbm_gbs if bound == "hbm" else nvl_gbs, 1),
             "peak": hbm_peak if bound == "hbm" else nvl_peak, "unit": "GB/s",
             "frac": round((hbm_gbs / hbm_peak) if bound == "hbm" else (nvl_gbs / nvl_peak), 4),
-            "traffic": None,
+            "traffic": traffic_for(args.config, world, dom),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if bound == "hbm" else
             "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
 

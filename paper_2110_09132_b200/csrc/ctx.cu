@@ -447,6 +447,13 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
   CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_main[p], 0));
   ctx->aux_used = ctx->side_used = true;
+  // the sort of this batch (aux stream) must be complete: a one-warp gate on a
+  // device flag the sort sets (a host event here would break the PDL chain);
+  // at N == 1 it also checks the prefetch fingerprints.  Enqueued before this
+  // backward's aux / side work so that host launch order is also a valid
+  // serial order (profilers replay kernels one at a time).
+  if (!ctx->fwd_sort_gated)
+    CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
   // finer-grained waits of the side stream on main-stream progress (device flags)
   auto seq_gate = [&](cudaStream_t s2, int si, int wi) {
     return run_k(ctx, EMB_K_GATE, s2, [&] { return launch_gate(ctx->dc, p, GATE_SEQ, (si << 8) | wi, s2); });
@@ -500,11 +507,6 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       ctx->sort_pending[p ^ 1] = true;
     }
   }
-  // the sort of this batch (aux stream) must be complete: a one-warp gate on a
-  // device flag the sort sets (a host event here would break the PDL chain);
-  // at N == 1 it also checks the prefetch fingerprints
-  if (!ctx->fwd_sort_gated)
-    CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
   ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
     CKC(ctx, run_k(ctx, EMB_K_RAWPUSH, stream, [&] { return launch_rawpush(c, lc, grad_out, last_n, p, stream); }));
