@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   __shared__ int ch[NB];            // this CTA's digit totals (read by the cluster)
   __shared__ int gs[NB];            // global start of (digit, this CTA)
   __shared__ int tmp[CS_WARPS];
-  __shared__ int xs[4];             // values exchanged over DSMEM: kept heads, kept tokens, chunks, long
+  __shared__ int xs[6];             // over DSMEM: kept heads, kept tokens, chunks, long, first head; queue
   __shared__ int wk[CS_WARPS];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -199,10 +199,13 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   int* perm = c.perm + bpn;
   int* uid = c.uid + bpn;
   int* useg = c.useg + pn(c, p, n) * (size_t)(c.max_tok + 1);
+  int* hpos = reinterpret_cast<int*>(keyB);  // segment starts of this CTA's uniques (keyB is free now)
   const K posmask = (K(1) << posbits) - 1;
   K prev_last = K(0);
   if (cr > 0 && cnt > 0) prev_last = *cluster.map_shared_rank(keyA + (S - 1), cr - 1);
-  int kept_heads = 0, kept_tok = 0;
+  if (tid == 0) xs[4] = 0x7fffffff;
+  __syncthreads();
+  int kept_heads = 0, kept_tok = 0, first_head = 0x7fffffff;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int i = w * EPW + r * 32 + lane;
@@ -214,15 +217,20 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
       keep = idp < L;
       const K prev = (i > 0) ? keyA[i - 1] : prev_last;
       head = keep && ((i == 0 && cr == 0) || (prev >> posbits) != (key >> posbits));
+      if (head) first_head = min(first_head, lo + i);
     }
     kept_heads += __popc(__ballot_sync(0xffffffffu, head));
     kept_tok += __popc(__ballot_sync(0xffffffffu, valid && keep));
   }
-  if (lane == 0) wk[w] = kept_heads;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first_head = min(first_head, __shfl_xor_sync(0xffffffffu, first_head, o));
+  if (lane == 0) {
+    wk[w] = kept_heads;
+    if (first_head != 0x7fffffff) atomicMin(&xs[4], first_head);
+  }
   {
     int tk_all;
-    const int tk_ex = cta_exscan(lane == 0 ? kept_tok : 0, tmp, &tk_all);
-    (void)tk_ex;
+    cta_exscan(lane == 0 ? kept_tok : 0, tmp, &tk_all);
     if (tid == 0) xs[1] = tk_all;
   }
   __syncthreads();
@@ -231,13 +239,18 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     for (int ww = 0; ww < CS_WARPS; ++ww) { const int x = wk[ww]; wk[ww] = run; run += x; }
     xs[0] = run;
   }
-  cluster.sync();  // xs[0] (kept heads) and xs[1] (kept tokens) of every CTA
+  cluster.sync();  // xs[0] (kept heads), xs[1] (kept tokens), xs[4] (first kept head) of every CTA
   int kb, U, tkb, Tk;
   cluster_exsum(cluster, &xs[0], cr, &kb, &U);
   cluster_exsum(cluster, &xs[1], cr, &tkb, &Tk);
   (void)tkb;
+  int next_first = Tk;  // end of this CTA's last segment: the next kept head, else the first dropped key
+  for (int q = CL - 1; q > cr; --q) {
+    const int f = *cluster.map_shared_rank(&xs[4], q);
+    if (f != 0x7fffffff) next_first = f;
+  }
   {
-    int kbase = kb + wk[w];
+    int kbase = wk[w];  // local unique index
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
       const int i = w * EPW + r * 32 + lane;
@@ -254,10 +267,12 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
       if (valid) {
         perm[lo + i] = (int)(key & posmask);
         if (head) {
-          const int k = kbase + __popc(hm & lt);
+          const int j = kbase + __popc(hm & lt);
+          const int k = kb + j;
           const int id = (int)(key >> posbits);
           uid[k] = id;
           useg[k] = lo + i;
+          hpos[j] = lo + i;
           if (c.N > 1) c.slotmap[((size_t)p * c.L + id) * c.N + n] = ((unsigned long long)tt << 32) | (unsigned)k;
         }
       }
@@ -265,18 +280,19 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     }
   }
   if (cr == 0 && tid == 0) useg[U] = Tk;  // end of the last kept segment (kept keys sort first)
-  cluster.sync();  // useg[] of the whole cluster is in global memory (release / acquire at cluster scope)
+  __syncthreads();  // hpos[] complete
 
   EMB_TR_AT(1, tt, 6);
   // ---- reduce chunks of C rows per unique: descriptors, multi-chunk list
+  //      (segment ends from hpos / next_first: no global round trip)
   int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
   int4* chunk_desc = c.chunk_desc + pn(c, p, n) * (size_t)c.max_chunks;
   int* long_u = c.long_u + pn(c, p, n) * (size_t)c.max_long;
   const int hc = xs[0];  // this CTA's uniques: [kb, kb + hc)
   int my_ch = 0, my_long = 0;
   for (int j = tid; j < hc; j += CS_THREADS) {
-    const int k = kb + j;
-    const int nch = (__ldcg(useg + k + 1) - __ldcg(useg + k) + c.C - 1) / c.C;
+    const int e = (j + 1 < hc) ? hpos[j + 1] : next_first;
+    const int nch = (e - hpos[j] + c.C - 1) / c.C;
     my_ch += nch;
     my_long += nch > 1;
   }
@@ -284,19 +300,22 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     int a, b;
     cta_exscan(my_ch, tmp, &a);
     cta_exscan(my_long, tmp, &b);
-    if (tid == 0) { xs[2] = a; xs[3] = b; }
+    if (tid == 0) { xs[2] = a; xs[3] = b; xs[5] = 0; }
   }
   cluster.sync();
   int cb, NCH, lb, NLONG;
   cluster_exsum(cluster, &xs[2], cr, &cb, &NCH);
   cluster_exsum(cluster, &xs[3], cr, &lb, &NLONG);
+  constexpr int QMAX = 32, QMIN = 8;  // uniques of > QMIN chunks: descriptors written by the whole CTA
+  __shared__ int4 lq[QMAX];
+  __shared__ int lq_off[QMAX];
   for (int j0 = 0; j0 < hc; j0 += CS_THREADS) {
     const int j = j0 + tid;
     const int k = kb + j;
     int a = 0, b = 0, nch = 0;
     if (j < hc) {
-      a = __ldcg(useg + k);
-      b = __ldcg(useg + k + 1);
+      a = hpos[j];
+      b = (j + 1 < hc) ? hpos[j + 1] : next_first;
       nch = (b - a + c.C - 1) / c.C;
     }
     int tch, tlong;
@@ -305,11 +324,26 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     if (j < hc) {
       const int off = cb + och;
       chunk_off[k] = off;
-      for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
+      int qs = -1;
+      if (nch > QMIN) {
+        qs = atomicAdd(&xs[5], 1);
+        if (qs < QMAX) {
+          lq[qs] = make_int4(k, a, b, nch);
+          lq_off[qs] = off;
+        }
+      }
+      if (qs < 0 || qs >= QMAX)
+        for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
       if (nch > 1) long_u[lb + olong] = k;
     }
     cb += tch;
     lb += tlong;
+  }
+  __syncthreads();
+  for (int e = 0; e < min(xs[5], QMAX); ++e) {  // Zipf-head uniques: descriptors by the whole CTA
+    const int4 u = lq[e];
+    for (int q = tid; q < u.w; q += CS_THREADS)
+      chunk_desc[lq_off[e] + q] = make_int4(u.x, u.y + q * c.C, min(u.z, u.y + (q + 1) * c.C), u.w);
   }
   if (cr == 0 && tid == 0) {
     chunk_off[U] = NCH;
