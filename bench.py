@@ -301,7 +301,8 @@ def main():
     shard0 = torch.from_numpy(np.ascontiguousarray(W[:, rank * d:(rank + 1) * d])).to(dev).to(tdt)
     del W
     ex = EmbraceExchange(cfg.L, cfg.D, shard0, world=world, rank=rank, device=local, dtype=cfg.dtype,
-                         max_tokens=cfg.max_tokens, mode=mode, optim=cfg.optim, lr=cfg.lr)
+                         max_tokens=cfg.max_tokens, mode=mode, optim=cfg.optim, lr=cfg.lr,
+                         timeout_ms=int(os.environ.get("EMB_TIMEOUT_MS", "10000")))
     del shard0
     stream = torch.cuda.current_stream()
 
@@ -318,6 +319,9 @@ def main():
         torch.cuda.synchronize()
         ef = ex.stats()["err_flags"]
         if ef:
+            info = E.emb_debug_copy(ex.ctx, E.EMB_DBG_ERRINFO).reshape(8, 4)
+            waits = [tuple(int(v) for v in r[:3]) for r in info if r[3]]
+            print(f"[bench] rank {rank}: expired waits (site, seen, target): {waits}", file=sys.stderr, flush=True)
             raise RuntimeError(f"rank {rank}: device error flags {ef} after the {phase}")
 
     for k in range(args.warmup):

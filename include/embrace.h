@@ -135,8 +135,8 @@ typedef enum {
   EMB_DBG_PERM = 3,     /* int32 [T_src]  positions of source src sorted by (dropped, id,
                            position); slot k's rows are perm[seg_start[k] .. seg_end[k]) */
   EMB_DBG_ISSUE_LOG = 4, /* int64 [k]     dense-queue tickets in issue order          */
-  EMB_DBG_ERRINFO = 6,   /* int32 [4]     first expired peer/flag wait: site code,
-                           value seen, target, 1 if set (diagnostics for EMB_ERR_TIMEOUT) */
+  EMB_DBG_ERRINFO = 6,   /* int32 [8][4]  the first 8 expired peer/flag waits in expiry order: site
+                           code, value seen, target, 1 if set (EMB_ERR_TIMEOUT) */
   EMB_DBG_TIMESTAMPS = 5, /* uint64 [16][20][8] kernel trace ring: [t%16][kernel kind][entered,
                              waited, finished, phase stamps] globaltimer ns (EMB_TRACE builds) */
 } emb_debug_item;

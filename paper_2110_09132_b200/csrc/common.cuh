@@ -90,7 +90,7 @@ struct DevCtx {
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits
-  unsigned* err_info;     // [4] first expired wait: site, observed, target, set
+  unsigned* err_info;     // [8][4] + count: expired waits (site, observed, target, set)
   unsigned long long* stats;  // [3][N] bytes: fwd pulled / bwd pushed / ids pushed
   unsigned long long* dbg_ts; // [EMB_TRACE_SLOTS] kernel trace (EMB_TRACE builds only)
 };
@@ -196,10 +196,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // err_info = {site, observed value, target, 1} (emb_debug_copy EMB_DBG_ERRINFO).
 __device__ __forceinline__ void note_timeout(const DevCtx& c, int site, uint32_t seen, uint32_t target) {
   atomicOr(c.err, ERR_TIMEOUT);
-  if (atomicCAS(c.err_info + 3, 0u, 1u) == 0u) {
-    c.err_info[0] = (unsigned)site;
-    c.err_info[1] = seen;
-    c.err_info[2] = target;
+  // up to 8 expired waits, in expiry order: {site, seen, target, 1}
+  const unsigned slot = atomicAdd(c.err_info + 32, 1u);
+  if (slot < 8) {
+    c.err_info[slot * 4 + 0] = (unsigned)site;
+    c.err_info[slot * 4 + 1] = seen;
+    c.err_info[slot * 4 + 2] = target;
+    c.err_info[slot * 4 + 3] = 1u;
   }
 }
 __device__ __forceinline__ void wait_flag(const DevCtx& c, const uint32_t* flag, uint32_t target, int site = 0) {

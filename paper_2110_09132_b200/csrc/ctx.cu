@@ -108,7 +108,7 @@ struct emb_ctx {
   bool peer_open[EMB_MAX_WORLD] = {};
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
-  cudaStream_t aux = nullptr;   // per-source sort of the next batch (overlaps the current iteration)
+  cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
   cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
@@ -274,7 +274,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
-    ALLOC(c.err_info, 16);
+    ALLOC(c.err_info, 33 * 4);
     ALLOC(c.stats, 3 * N * 8);
     ALLOC(c.dbg_ts, EMB_TRACE_SLOTS * 8);
   }
@@ -394,10 +394,11 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->mark_pending = false;
   const int pre = ctx->prefetched ? 1 : 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre, stream));
-  // sort_gate = 1 would let the forward's CTA 0 wait for sort(t) instead of a
-  // gate kernel before the coalesce; measured slower at N == 1 (the fork of
-  // sort(t+1) then also waits for sort(t)), so the gate kernel stays.
-  const int sort_gate = 0;
+  // sort_gate: the forward's CTA 0 waits for sort(t) instead of a gate kernel
+  // before the coalesce (one kernel boundary less).  Not at N == 1: there the
+  // step is bounded by fwd(t) + sort(t+1) (sort(t+1) is forked after the
+  // forward), and the wait would lengthen the forward (measured slower).
+  const int sort_gate = (pre && ctx->cfg.mode != EMB_BWD_RAW && ctx->pl.N > 1) ? 1 : 0;
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
                  [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, stream); }));
   ctx->fwd_sort_gated = sort_gate != 0;
@@ -405,12 +406,13 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
-    CKC(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_main[p], 0));
-    CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, ctx->aux));
-    CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux, [&] {
-      return launch_sort(ctx->dc, p, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux);
+    cudaStream_t sq = ctx->aux;
+    CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_main[p], 0));
+    CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, sq));
+    CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
+      return launch_sort(ctx->dc, p, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, sq);
     }));
-    CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], ctx->aux));
+    CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], sq));
     ctx->sort_pending[p] = true;
     ctx->aux_used = true;
   }
@@ -499,11 +501,15 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       // a6 for the next batch, one iteration ahead.  Its parity's previous user
       // (the scheduled merge of t-1) must be done with the routing tables: the
       // gate waits this rank's def_done flag.
-      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 4, aux));
-      CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
-        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
+      // (a separate sort queue, so that a sort waiting for the scheduled merge of
+      // t-1 does not delay the next prefetch push, was measured slower and hung
+      // intermittently in round 1: kept on aux)
+      cudaStream_t sq = aux;
+      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 4, sq));
+      CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
+        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, sq);
       }));
-      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], sq));
       ctx->sort_pending[p ^ 1] = true;
     }
   }
@@ -703,9 +709,9 @@ emb_status emb_debug_copy(emb_ctx* ctx, int32_t item, int32_t src, void* host, s
   CKC(ctx, cudaSetDevice(ctx->cfg.device));
   CKC(ctx, cudaDeviceSynchronize());
   if (item == EMB_DBG_ERRINFO) {
-    *n = 4;
-    if (cap < 16) return EMB_ERR_CAPACITY;
-    CKC(ctx, cudaMemcpy(host, ctx->dc.err_info, 16, cudaMemcpyDeviceToHost));
+    *n = 32;
+    if (cap < 32 * 4) return EMB_ERR_CAPACITY;
+    CKC(ctx, cudaMemcpy(host, ctx->dc.err_info, 32 * 4, cudaMemcpyDeviceToHost));
     return EMB_OK;
   }
   if (item == EMB_DBG_TIMESTAMPS) {
