@@ -74,6 +74,9 @@ struct DevCtx {
   int4* chunk_desc;       // [2][N][max_chunks] chunk -> {unique i, perm begin, perm end, chunks of i}
   int* long_u;            // [2][N][max_long]   uniques with more than one chunk
   int* slot_id;           // [2][N][max_tok]    Alg. 1 slot order (prior asc, then scheduled asc) — tables
+  int* plan;              // [2][2 parts][N*max_tok][1+N] owner merge plan: id, then the unique index of
+                          //   the id at every source (-1: absent); one entry per distinct id (N > 1)
+  int* plan_cnt;          // [2][2]  entries per part
   int* counts;            // [2][N][CNT_W]
   float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
   int* slot_ctr;          // [2][N][max_tok]    (unused; reserved)

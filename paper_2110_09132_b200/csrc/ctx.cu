@@ -255,6 +255,8 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.uid, 2 * N * T * 4);
     ALLOC(c.useg, 2 * N * (T + 1) * 4);
     ALLOC(c.slot_id, 2 * N * T * 4);
+    if (N > 1) ALLOC(c.plan, 2 * 2 * N * T * (1 + N) * 4);
+    ALLOC(c.plan_cnt, 2 * 2 * 4);
     ALLOC(c.chunk_off, 2 * N * (T + 1) * 4);
     ALLOC(c.chunk_desc, 2 * N * (size_t)pl.max_chunks * 16);
     if (cfg->mode != EMB_BWD_RAW) ALLOC(c.gcoal, T * cfg->dim * 4);
@@ -393,15 +395,18 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // the main stream reads it (the prefetch check is a fingerprint, k_gate.cu)
   ctx->mark_pending = false;
   const int pre = ctx->prefetched ? 1 : 0;
-  CKC(ctx, gate(ctx, p, GATE_FWD, pre, stream));
-  // sort_gate: the forward's CTA 0 waits for sort(t) instead of a gate kernel
-  // before the coalesce (one kernel boundary less).  Not at N == 1: there the
-  // step is bounded by fwd(t) + sort(t+1) (sort(t+1) is forked after the
-  // forward), and the wait would lengthen the forward (measured slower).
-  const int sort_gate = (pre && ctx->cfg.mode != EMB_BWD_RAW && ctx->pl.N > 1) ? 1 : 0;
+  // N > 1 and prefetched: GATE_FWD also waits for sort(t) (computed one
+  // iteration ahead), and the forward pulls each distinct row once (dedup)
+  // using the sort's chunk descriptors; the coalesce then needs no sort gate.
+  // N == 1: the step is bounded by fwd(t) + sort(t+1) (sort(t+1) is forked
+  // after the forward), so the forward must not wait for the sort there
+  // (sort_gate = 1, CTA 0 waiting at the forward's end, measured slower).
+  const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
+  const int sort_gate = 0;
+  CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
-                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, stream); }));
-  ctx->fwd_sort_gated = sort_gate != 0;
+                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, dedup, stream); }));
+  ctx->fwd_sort_gated = dedup != 0;
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
@@ -479,7 +484,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     }
     CKC(ctx, seq_gate(side, SEQ_BWD, W_SIDE));  // also orders after sort(t) (GATE_SORTED waited it)
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_markpush(c, p, next_ids, n_next, side); }));
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, 1, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
     ctx->mark_pending = true;
     CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, side); }));
@@ -491,27 +496,23 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // a5 on the aux stream: the prefetch push of ids(t+1) and the D_next tags
     // overlap the segmented reduce (which does not need them); only the apply,
     // which routes prior vs scheduled rows, waits for them (GATE_MARKED).
+    // aux chain (critical at N > 1: the forward of t+1 dedups with sort(t+1)):
+    // push ids(t+1) -> one gate (publish + wait ids(t+1), and this rank's
+    // scheduled push of t-1 past the routing tables) -> D_next tags -> merge
+    // plan -> sort(t+1) -> the Alg. 1 tables of t (presentation, last).
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, aux); }));
-    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2, aux));  // publish + wait ids(t+1)
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, aux); }));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4, aux));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, aux); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;
-    // a8 presentation (P_n ++ D_n slot tables, p_n): off the critical path
-    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
     if (next_ids) {
-      // a6 for the next batch, one iteration ahead.  Its parity's previous user
-      // (the scheduled merge of t-1) must be done with the routing tables: the
-      // gate waits this rank's def_done flag.
-      // (a separate sort queue, so that a sort waiting for the scheduled merge of
-      // t-1 does not delay the next prefetch push, was measured slower and hung
-      // intermittently in round 1: kept on aux)
-      cudaStream_t sq = aux;
-      CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 4, sq));
-      CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
-        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, sq);
+      CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
+        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
       }));
-      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], sq));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
       ctx->sort_pending[p ^ 1] = true;
     }
+    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
   }
   ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
@@ -520,8 +521,13 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_RAWCOAL, stream, [&] { return launch_rawcoal(c, lc, p, stream); }));
     CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
   } else {
-    const int cg = (N == 1 ? 1 : 0) | (mode == EMB_BWD_SPLIT && N > 1 ? 2 : 0);
+    // (SPLIT, N > 1: the D_next tags of t+1 must be complete before the apply
+    // routes rows; a one-warp gate, not the reduce kernel's CTA 0: a wide
+    // kernel spinning on a flag was observed to hold back the launch of the
+    // aux-stream kernel that sets it — timeouts)
+    const int cg = (N == 1 ? 1 : 0);
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, cg, stream); }));
+    if (mode == EMB_BWD_SPLIT) CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
     CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.

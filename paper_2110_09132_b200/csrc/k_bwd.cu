@@ -624,48 +624,33 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
   pdl_wait();
   constexpr int EPV = Vec<DT>::EPV;
   const uint32_t t = c.t_rec[p];
+  (void)t;
   EMB_TR_BEGIN(part ? 6 : 4, t);
   // N > 1: every sender's pass of this part completed (the gate before this
-  // kernel waited for their pub flags)
-  int cnt[EMB_WMAX];
-  int total = 0;
-#pragma unroll
-  for (int n = 0; n < EMB_WMAX; ++n) {
-    cnt[n] = (n < c.N) ? counts_of(c, p, n)[CNT_U] : 0;
-    total += cnt[n];
-  }
+  // kernel waited for their pub flags).  Items: this part's plan entries (one
+  // per distinct id: the id and its unique index at every source, plan_kernel).
+  // N == 1 (RAW mode only): one source, every unique is its own leader
+  const int total = (c.N == 1) ? counts_of(c, p, 0)[CNT_U] : c.plan_cnt[p * 2 + part];
+  const int PW = 1 + c.N;
+  const int* plan = (c.N == 1) ? nullptr : c.plan + ((size_t)p * 2 + part) * c.N * c.max_tok * PW;
   const float alpha = (c.optim == ADAM) ? c.alpha[p] : 0.f;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int grp = gtid / G, gl = gtid - grp * G, ngrp = (gridDim.x * blockDim.x) / G;
   const size_t slice_bytes = (size_t)c.d * c.esz;
   char* shard = shard_of(c, c.r);
-  const bool split = (c.mode == SPLIT);
   for (int item = grp; item < total; item += ngrp) {
-    int n = 0, rem = item;
+    int u, ks[EMB_WMAX];
+    if (c.N == 1) {
+      u = c.uid[pn(c, p, 0) * (size_t)c.max_tok + item];
+      ks[0] = item;
 #pragma unroll
-    for (int m = 0; m < EMB_WMAX - 1; ++m)
-      if (n == m && rem >= cnt[m]) { rem -= cnt[m]; n = m + 1; }
-    const int k = rem;
-    const int u = c.uid[pn(c, p, n) * (size_t)c.max_tok + k];
-    if (split) {
-      const bool pr = is_prior(c, p, t, u);
-      if (pr != (part == 0)) continue;  // the other part's row
-    }
-    unsigned long long ent[EMB_WMAX];
-    bool leader = true;
-    if (c.N > 1) {
-      const unsigned long long* sm = c.slotmap + ((size_t)p * c.L + u) * c.N;
-#pragma unroll
-      for (int n2 = 0; n2 < EMB_WMAX; ++n2) {
-        ent[n2] = (n2 < c.N) ? sm[n2] : 0ull;
-        if (n2 < n && (uint32_t)(ent[n2] >> 32) == t) leader = false;
-      }
+      for (int n2 = 1; n2 < EMB_WMAX; ++n2) ks[n2] = -1;
     } else {
+      const int* e = plan + (size_t)item * PW;
+      u = e[0];
 #pragma unroll
-      for (int n2 = 0; n2 < EMB_WMAX; ++n2) ent[n2] = 0ull;
-      ent[0] = ((unsigned long long)t << 32) | (unsigned)k;
+      for (int n2 = 0; n2 < EMB_WMAX; ++n2) ks[n2] = (n2 < c.N) ? e[1 + n2] : -1;
     }
-    if (!leader) continue;  // the lowest source holding u applies it
     for (int c16 = gl; c16 < c.cps; c16 += G) {
       // state loads first (independent of the contributions)
       char* wp = shard + (size_t)u * slice_bytes + (size_t)c16 * 16;
@@ -686,9 +671,9 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
 #pragma unroll
       for (int i = 0; i < EPV; ++i) g[i] = 0.f;
 #pragma unroll
-      for (int n2 = 0; n2 < EMB_WMAX; ++n2) {  // ascending source rank
-        if (n2 >= n && n2 < c.N && (uint32_t)(ent[n2] >> 32) == t) {
-          const int k2 = (int)(uint32_t)ent[n2];
+      for (int n2 = 0; n2 < EMB_WMAX; ++n2) {  // ascending source rank (reading R12)
+        if (ks[n2] >= 0) {
+          const int k2 = ks[n2];
           float f[EPV];
           if (RAWSRC) {
             const float* src = c.gc_owner + (pn(c, p, n2) * (size_t)c.max_tok + k2) * c.d + c16 * EPV;

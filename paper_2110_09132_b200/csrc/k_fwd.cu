@@ -26,7 +26,7 @@ static constexpr int FWD_ROWS = 4;  // rows in flight per warp
 template <int V>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* __restrict__ ids, int n,
                                                           char* __restrict__ out, int p, int prefetched,
-                                                          int sort_gate) {
+                                                          int sort_gate, int dedup) {
   EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
@@ -84,6 +84,62 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     src_base[v] = (c16 < c.cpr) ? shard_of(c, s) : nullptr;
     src_off[v] = (c16 - s * c.cps) * 16;
   }
+  if (dedup) {
+    // N > 1, prefetched: the sort of this batch is complete (GATE_FWD waited
+    // it), so every distinct row is pulled once per reduce chunk (<= C equal
+    // ids, ascending positions) and stored to all of the chunk's positions —
+    // the NVLink bytes of the forward drop from T_r to ~(U_r + Zipf-head chunks)
+    // rows (forward dedup).  Dropped keys (pad when
+    // pad_id >= 0, out-of-range ids) sort last and are gathered one by one.
+    const size_t bpn = pn(c, p, c.r) * (size_t)c.max_tok;
+    const int* cnt = counts_of(c, p, c.r);
+    const int NCH = cnt[CNT_NCH], U = cnt[CNT_U];
+    const int4* desc = c.chunk_desc + pn(c, p, c.r) * (size_t)c.max_chunks;
+    const int* perm = c.perm + bpn;
+    const int* uid = c.uid + bpn;
+    const int tail0 = c.useg[pn(c, p, c.r) * (size_t)(c.max_tok + 1) + U];
+    const int ntail = n - tail0;
+    const int items = NCH + (ntail + 31) / 32;
+    for (int it = gw; it < items; it += nw) {
+      if (it < NCH) {
+        const int4 dsc = desc[it];  // {unique, perm begin, perm end, chunks}
+        const int id = __ldg(uid + dsc.x);
+        const int j = dsc.y + lane;
+        const int mypos = (j < dsc.z) ? __ldg(perm + j) : 0;
+        uint4 buf[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          buf[v] = (src_base[v] != nullptr) ? ld16_nc(src_base[v] + (size_t)id * slice_bytes + src_off[v])
+                                            : make_uint4(0, 0, 0, 0);
+        for (int q = 0; q < dsc.z - dsc.y; ++q) {
+          const int pos = __shfl_sync(0xffffffffu, mypos, q);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int c16 = lane + 32 * v;
+            if (c16 < c.cpr) st16(out + (size_t)pos * row_bytes + (size_t)c16 * 16, buf[v]);
+          }
+        }
+      } else {
+        const int j = tail0 + (it - NCH) * 32 + lane;
+        const int mypos = (j < n) ? __ldg(perm + j) : -1;
+        const int myid = (mypos >= 0) ? __ldg(ids + mypos) : 0;
+        for (int q = 0; q < 32; ++q) {
+          const int pos = __shfl_sync(0xffffffffu, mypos, q);
+          const int id = __shfl_sync(0xffffffffu, myid, q);
+          if (pos < 0) break;
+          const bool ok = (unsigned)id < (unsigned long long)c.L;
+          if (!ok && lane == 0) atomicOr(c.err, ERR_ID);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int c16 = lane + 32 * v;
+            uint4 x = make_uint4(0, 0, 0, 0);
+            if (ok && src_base[v] != nullptr) x = ld16_nc(src_base[v] + (size_t)id * slice_bytes + src_off[v]);
+            if (c16 < c.cpr) st16(out + (size_t)pos * row_bytes + (size_t)c16 * 16, x);
+          }
+        }
+      }
+    }
+  } else
   for (int j0 = gw * FWD_ROWS; j0 < n; j0 += nw * FWD_ROWS) {
     int id[FWD_ROWS];
 #pragma unroll
@@ -124,7 +180,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
 }
 
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, int sort_gate, cudaStream_t s) {
+                       int prefetched, int sort_gate, int dedup, cudaStream_t s) {
   const int warps = (n + FWD_ROWS - 1) / FWD_ROWS;
   int grid = (warps + FWD_THREADS / 32 - 1) / (FWD_THREADS / 32);
   if (grid < 1) grid = 1;
@@ -132,10 +188,10 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   const int V = (c.cpr + 31) / 32;
   char* o = static_cast<char*>(out);
   const dim3 g(grid), b(FWD_THREADS);
-  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
-  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
-  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
-  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate);
+  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
+  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
+  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
+  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
   return cudaErrorInvalidValue;
 }
 

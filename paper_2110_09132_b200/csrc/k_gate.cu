@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         Flags* f = flags_of(c, c.r);
         wait_all(c, f->prior_done, t - 1, 1);
         wait_all(c, f->def_done, t - 2, 2);
-        if (flag_arg) wait_local(c, c.marked + (p ^ 1), t - 1, 3);  // the prefetch copy this forward checks
+        if (flag_arg & 1) wait_local(c, c.marked + (p ^ 1), t - 1, 3);  // the prefetch copy this forward checks
+        if (flag_arg & 2) wait_local(c, c.sorted + p, t, 3 * 16 + 1);    // the forward dedups with sort(t)
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -47,13 +48,14 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // ids of batch tt (parity p).  flag_arg bits: 1 = the predecessor (the
         // forward or markpush) pushed this rank's ids: publish them; 2 = wait
         // for every source's ids; 4 (SPLIT) = the routing tables of parity p are
-        // free once this rank's scheduled merge of tt-2 (side stream) is done.
+        // free once this rank's scheduled push of tt-2 (side stream) is past.
         const uint32_t tt = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, tt);
         if (flag_arg & 1) publish(c, EMB_FLAG_OFF(ids), tt);
         if (flag_arg & 2) wait_all(c, flags_of(c, c.r)->ids, tt, 4);
-        if ((flag_arg & 4) && c.mode == SPLIT && tt >= 3)
-          wait_flag(c, &flags_of(c, c.r)->def_done[c.r], tt - 2, 5 * 16);
+        // (the scheduled merge reads the merge plan, not the routing tables, so
+        // only this rank's scheduled push of tt-2 must be past them)
+        if ((flag_arg & 4) && c.mode == SPLIT && tt >= 3) wait_local(c, c.seq + SEQ_DEFPUSHED, tt - 2, 5 * 16);
         EMB_TR_END(10 + kind, tt);
         break;
       }
@@ -64,9 +66,11 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
         const int part = (kind == GATE_PUB1) ? 1 : 0;
-        if (!part) st_release_gpu(c.seq + SEQ_APPLIED, t);  // the apply of t completed (side stream waits)
+        if (!part) st_release_gpu(c.seq + SEQ_APPLIED, t);     // the apply of t completed (side stream waits)
+        else st_release_gpu(c.seq + SEQ_DEFPUSHED, t);          // defpush(t) no longer needs the routing tables
         publish(c, part ? EMB_FLAG_OFF(pub[1]) : EMB_FLAG_OFF(pub[0]), t);
         wait_all(c, flags_of(c, c.r)->pub[part], t, 6 + part);
+        if (!part) wait_local(c, c.marked + p, t, 8 * 16 + 2);  // the merge plan of t (aux stream) is complete
         EMB_TR_END(10 + kind, t);
         break;
       }

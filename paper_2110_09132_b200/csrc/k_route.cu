@@ -116,11 +116,12 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
 // ids flags), tag D_next: nextmark[p][id] = t+1 (epoch tag, never cleared), so
 // the split is a per-id test everywhere.  Then the completion flag marked[p].
 static constexpr int MT_CTAS_PER_SRC = 8;
-__global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark) {
+__global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark, int set_flag) {
   EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p];
   EMB_TR_BEGIN(17, t);
+  if (blockIdx.x == 0 && threadIdx.x < 2) c.plan_cnt[p * 2 + threadIdx.x] = 0;  // re-arm the plan of parity p
   if (do_mark) {
     int* mark = c.nextmark + (size_t)p * c.L;
     const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -140,9 +141,10 @@ __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, in
       }
     }
   }
-  // completion flag for the gates of the main stream (the apply, the next forward)
+  // completion flag for the gates of the main stream (the apply, the next
+  // forward); N > 1 the plan kernel that follows sets it instead
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (set_flag && threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&c.mark_cnt[p], 1u) == gridDim.x - 1) {
       c.mark_cnt[p] = 0;
@@ -151,6 +153,68 @@ __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, in
     }
   }
   EMB_TR_END(17, t);
+  pdl_trigger();
+}
+
+// ============================================================== owner merge plan (N > 1)
+// Thread per (source n, unique i): the lowest source holding the id (slotmap
+// tag == t) emits one plan entry {id, i at every source or -1} into the part
+// of the id (SPLIT: prior iff in D_next).  The merge kernels then walk their
+// part's entries: no slotmap / D_next lookups and no idle items on the
+// critical path, and the scheduled merge no longer reads the routing tables
+// (so the sort of t+1 only waits for this rank's scheduled push of t-1).
+__global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
+  EMB_TR_ENTRY();
+  pdl_wait();
+  const uint32_t t = c.t_rec[p];
+  EMB_TR_BEGIN(19, t);
+  int cnt[EMB_WMAX];
+  int total = 0;
+#pragma unroll
+  for (int n = 0; n < EMB_WMAX; ++n) {
+    cnt[n] = (n < c.N) ? counts_of(c, p, n)[CNT_U] : 0;
+    total += cnt[n];
+  }
+  const int PW = 1 + c.N;
+  for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < total; item += gridDim.x * blockDim.x) {
+    int n = 0, k = item;
+#pragma unroll
+    for (int m = 0; m < EMB_WMAX - 1; ++m)
+      if (n == m && k >= cnt[m]) { k -= cnt[m]; n = m + 1; }
+    const int u = c.uid[pn(c, p, n) * (size_t)c.max_tok + k];
+    const unsigned long long* sm = c.slotmap + ((size_t)p * c.L + u) * c.N;
+    int ks[EMB_WMAX];
+    bool leader = true;
+#pragma unroll
+    for (int n2 = 0; n2 < EMB_WMAX; ++n2) {
+      ks[n2] = -1;
+      if (n2 < c.N) {
+        const unsigned long long e = (n2 == n) ? (((unsigned long long)t << 32) | (unsigned)k) : sm[n2];
+        if ((uint32_t)(e >> 32) == t) {
+          ks[n2] = (int)(uint32_t)e;
+          if (n2 < n) leader = false;
+        }
+      }
+    }
+    if (!leader) continue;
+    const int part = (c.mode == SPLIT && !is_prior(c, p, t, u)) ? 1 : 0;
+    const int slot = atomicAdd(&c.plan_cnt[p * 2 + part], 1);
+    int* e = c.plan + (((size_t)p * 2 + part) * c.N * c.max_tok + slot) * PW;
+    e[0] = u;
+#pragma unroll
+    for (int n2 = 0; n2 < EMB_WMAX; ++n2)
+      if (n2 < c.N) e[1 + n2] = ks[n2];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // completion flag (marked[p]: D_next tags and plan are complete)
+    __threadfence();
+    if (atomicAdd(&c.mark_cnt[p], 1u) == gridDim.x - 1) {
+      c.mark_cnt[p] = 0;
+      __threadfence();
+      st_release_gpu(&c.marked[p], t);
+    }
+  }
+  EMB_TR_END(19, t);
   pdl_trigger();
 }
 
@@ -234,8 +298,15 @@ cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_n
   return launch_pdl(markpush_kernel, dim3(c.N * MP_SLICES), dim3(MP_THREADS), 0, s, c, p, next_ids, n_next);
 }
 
-cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, cudaStream_t s) {
-  return launch_pdl(marktag_kernel, dim3(c.N * MT_CTAS_PER_SRC), dim3(MP_THREADS), 0, s, c, p, do_mark);
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, cudaStream_t s) {
+  return launch_pdl(marktag_kernel, dim3(c.N * MT_CTAS_PER_SRC), dim3(MP_THREADS), 0, s, c, p, do_mark, set_flag);
+}
+
+cudaError_t launch_plan(const DevCtx& c, int p, cudaStream_t s) {
+  long long items = (long long)c.N * c.max_tok;
+  int grid = (int)((items + MP_THREADS - 1) / MP_THREADS);
+  if (grid > 148 * 4) grid = 148 * 4;
+  return launch_pdl(plan_kernel, dim3(grid), dim3(MP_THREADS), 0, s, c, p);
 }
 
 cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
@@ -247,7 +318,8 @@ cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
 }
 
 cudaError_t preload_route() {
-  for (const void* f : {(const void*)markpush_kernel, (const void*)marktag_kernel, (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
+  for (const void* f : {(const void*)markpush_kernel, (const void*)marktag_kernel, (const void*)plan_kernel,
+                        (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
                         (const void*)tables_kernel<4>, (const void*)tables_kernel<5>, (const void*)tables_kernel<8>,
                         (const void*)tables_kernel<12>, (const void*)tables_kernel<16>})
     if (cudaError_t e = preload(f)) return e;

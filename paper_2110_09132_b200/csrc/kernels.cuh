@@ -77,14 +77,14 @@ enum GateKind {
   GATE_DEFDONE = 6,  // side, after merge(part 1): publish def_done(t) to every owner
   GATE_SEQ = 7       // aux / side: wait for the next main-stream step (flag_arg = seq << 8 | waiter)
 };
-enum SeqIndex { SEQ_BWD = 0, SEQ_APPLIED = 1 };
+enum SeqIndex { SEQ_BWD = 0, SEQ_APPLIED = 1, SEQ_DEFPUSHED = 2 };
 enum SeqWaiter { W_AUX = 0, W_SIDE = 1 };
 cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s);
 
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
 // id push or prefetch check, wait for every owner, pull-gather)
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, int sort_gate, cudaStream_t s);
+                       int prefetched, int sort_gate, int dedup, cudaStream_t s);
 // a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
 // owner routing (slotmap) — auxiliary stream, one iteration ahead
 cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
@@ -94,7 +94,10 @@ cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
 // a5: prefetch all-gather of the next ids (markpush) and the D_next epoch tags
 // (marktag, + completion flag marked[p]) — Alg. 1 line 4's set
 cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, cudaStream_t s);
-cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, cudaStream_t s);
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, cudaStream_t s);
+// N > 1, after marktag: the owner merge plan of both parts (leaders, sources'
+// unique indices), then the completion flag marked[p]
+cudaError_t launch_plan(const DevCtx& c, int p, cudaStream_t s);
 // a8 presentation: Alg. 1 slot tables P_n ++ D_n, counts p_n (stats / debug; off the critical path)
 cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s);
 // a7 + a9 (+a10 for the prior part): sender coalesce — segmented reduce in
