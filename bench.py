@@ -308,6 +308,9 @@ def main():
 
     def step(k):
         b = k % nb
+        # the paper's prefetch: the next batch's ids are in memory before this
+        # step starts; emb_prefetch lets its work overlap the forward
+        E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], stream)
         E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], stream)
         E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], stream)
 
@@ -460,6 +463,7 @@ def main():
         nxt.copy_(h_ids[bn], non_blocking=True)
         dY_buf[:n].copy_(h_dY[b], non_blocking=True)
         h2d += nn * 4 + h_dY[b].numel() * h_dY[b].element_size()
+        E.emb_prefetch(ex.ctx, nxt, stream)
         E.emb_forward_exchange(ex.ctx, cur, Y_buf[:n], stream)
         E.emb_backward_exchange(ex.ctx, dY_buf[:n], nxt, stream)
         h_Y[b].copy_(Y_buf[:n], non_blocking=True)
@@ -473,6 +477,7 @@ def main():
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_tok = sum(int((np.asarray(ids_all[(kk + j) % nb][s]) != PAD_ID).sum()) for j in range(Ke) for s in range(world))
+    check_err("end-to-end pass")
     ex.flush()
     err = ex.stats()["err_flags"]
 

@@ -199,6 +199,18 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
  * receives one optimizer step with g = grad_scale * sum over ranks of its dY
  * rows.  SPLIT: rows in D_next are updated on `stream`; the rest on the side
  * stream, complete before forward(t+2) and at emb_flush.  Collective.       */
+/* Optional: the paper's prefetch ("always keep the data of
+ * the next iteration in memory") as an explicit point in the stream.  Call it
+ * after backward(t-1) and before forward(t) with the ids of iteration t+1
+ * (the same device pointer and count later passed to backward(t) as
+ * next_ids), once their values are in place in stream order.  The library
+ * then starts the next batch's prefetch push, sort and D_next tags at this
+ * point — concurrently with forward(t) — instead of at backward(t).  Without
+ * it, everything still works; the work just starts at backward(t).
+ *   errors: EMB_ERR_STATE if called between a forward and its backward or
+ *           twice; EMB_ERR_CAPACITY if n_next > max_tokens.                  */
+emb_status emb_prefetch(emb_ctx* ctx, const int32_t* next_ids, int32_t n_next, emb_stream_t stream);
+
 emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32_t* next_ids,
                                  int32_t n_next, emb_stream_t stream);
 

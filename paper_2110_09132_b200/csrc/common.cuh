@@ -90,6 +90,7 @@ struct DevCtx {
   unsigned int* mark_cnt; // [2]   CTAs of the running mark that finished (re-armed by the last)
   unsigned int* seq;      // [4]   main-stream progress: [SEQ_BWD] = t past gate_sorted, [SEQ_APPLIED] = t past apply
   unsigned int* seen;     // [4]   per waiting stream: how many of those steps it has consumed
+  unsigned int* fwd_dd;   // [2]   N > 1: the forward of parity p dedups (sort(t) was already complete at its gate)
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits

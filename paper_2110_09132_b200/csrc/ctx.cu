@@ -120,6 +120,11 @@ struct emb_ctx {
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
   bool fwd_sort_gated = false;  // the last forward's CTA 0 waited for sort(t) (no GATE_SORTED needed)
+  // emb_prefetch: fork point of the next batch's work, recorded before forward(t)
+  const int32_t* pf_ids = nullptr;
+  int32_t pf_n = -1;
+  bool pf_armed = false;
+  cudaEvent_t ev_pre = nullptr;
   bool fwd_pushed = false;   // last forward pushed its ids (route publishes them)
   int last_n = 0;
   DenseQueue* dq = nullptr;
@@ -273,6 +278,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.mark_cnt, 2 * 4);
     ALLOC(c.seq, 4 * 4);
     ALLOC(c.seen, 4 * 4);
+    ALLOC(c.fwd_dd, 2 * 4);
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
@@ -300,6 +306,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cudaEventCreateWithFlags(&ctx->ev_tables[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
   }
   if (cudaEventCreateWithFlags(&ctx->ev_marked, cudaEventDisableTiming) != cudaSuccess) goto fail;
+  if (cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_aux, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_side, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
@@ -401,12 +408,16 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // N == 1: the step is bounded by fwd(t) + sort(t+1) (sort(t+1) is forked
   // after the forward), so the forward must not wait for the sort there
   // (sort_gate = 1, CTA 0 waiting at the forward's end, measured slower).
+  //   The gate does not wait for sort(t): it only records whether sort(t) is
+  //   already complete (fwd_dd[p]); the forward dedups if so, else it gathers
+  //   every token (identical Y).  Waiting would put the aux chain (push, tags,
+  //   plan, sort) on the critical path when the sort is the slower side (LM).
   const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
   const int sort_gate = 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
                  [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, dedup, stream); }));
-  ctx->fwd_sort_gated = dedup != 0;
+  ctx->fwd_sort_gated = false;
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
@@ -424,6 +435,19 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   ctx->prefetched = false;
   ctx->last_n = n;
   ctx->state = ST_AFTER_FWD;
+  return EMB_OK;
+}
+
+emb_status emb_prefetch(emb_ctx* ctx, const int32_t* next_ids, int32_t n_next, emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (ctx->state == ST_AFTER_FWD || ctx->state == ST_CREATED || ctx->pf_armed) return EMB_ERR_STATE;
+  if (!next_ids || n_next < 0) return EMB_ERR_INVALID_ARG;
+  if (n_next > ctx->cfg.max_tokens) return EMB_ERR_CAPACITY;
+  CKC(ctx, cudaEventRecord(ctx->ev_pre, reinterpret_cast<cudaStream_t>(stream_)));
+  ctx->pf_ids = next_ids;
+  ctx->pf_n = n_next;
+  ctx->pf_armed = true;
   return EMB_OK;
 }
 
@@ -450,9 +474,14 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // record on the main stream does not break its programmatic-launch chain; a
   // wait on the main stream would, so every join back into it is a device
   // flag gate instead (GATE_SORTED, GATE_MARKED, GATE_FWD's def_done).
+  //   With emb_prefetch(next_ids) called before this step's forward, the fork
+  //   point is that earlier position (the next batch's work overlaps forward(t)).
+  const bool early = ctx->pf_armed && ctx->pf_ids == next_ids && ctx->pf_n == n_next && next_ids != nullptr;
+  ctx->pf_armed = false;
+  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 3;  // debug: 1 aux, 2 side
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
-  CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_main[p], 0));
-  CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_main[p], 0));
+  CKC(ctx, cudaStreamWaitEvent(aux, (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p], 0));
+  CKC(ctx, cudaStreamWaitEvent(side, (early && (pf_mode & 2)) ? ctx->ev_pre : ctx->ev_main[p], 0));
   ctx->aux_used = ctx->side_used = true;
   // the sort of this batch (aux stream) must be complete: a one-warp gate on a
   // device flag the sort sets (a host event here would break the PDL chain);
@@ -461,10 +490,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // serial order (profilers replay kernels one at a time).
   if (!ctx->fwd_sort_gated)
     CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
-  // finer-grained waits of the side stream on main-stream progress (device flags)
-  auto seq_gate = [&](cudaStream_t s2, int si, int wi) {
-    return run_k(ctx, EMB_K_GATE, s2, [&] { return launch_gate(ctx->dc, p, GATE_SEQ, (si << 8) | wi, s2); });
-  };
+
   if (N == 1) {
     // N == 1: nothing on the critical path needs the D_next marks (the coalesce
     // applies every row), so
@@ -482,7 +508,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       ctx->sort_pending[p ^ 1] = true;
       ctx->tables_pending[p ^ 1] = false;
     }
-    CKC(ctx, seq_gate(side, SEQ_BWD, W_SIDE));  // also orders after sort(t) (GATE_SORTED waited it)
+    // tables(t) reads sort(t)'s unique lists: an event join from aux into side
+    // (joins into side do not touch the main stream's programmatic chain; a
+    // spinning side gate started before the forward was observed to hold back
+    // the main stream's launches — timeouts)
+    if (ctx->sort_pending[p]) CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_sorted[p], 0));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_markpush(c, p, next_ids, n_next, side); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, 1, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
@@ -501,7 +531,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // scheduled push of t-1 past the routing tables) -> D_next tags -> merge
     // plan -> sort(t+1) -> the Alg. 1 tables of t (presentation, last).
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, aux); }));
-    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4, aux));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4 | 8, aux));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, aux); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;
@@ -531,14 +561,16 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.
+    if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));  // apply done
     if (ctx->pl.N > 1) {
       CKC(ctx, gate(ctx, p, GATE_PUB0, 0, stream));
       CKC(ctx, run_k(ctx, EMB_K_MERGE0, stream, [&] { return launch_merge(c, lc, p, 0, stream); }));
     }
     if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) {
       // scheduled part: lowest-priority side stream, once the apply of t staged
-      // the scheduled rows (sequence flag set by GATE_PUB0)
-      CKC(ctx, seq_gate(side, SEQ_APPLIED, W_SIDE));
+      // the scheduled rows: an event recorded on the main stream after the
+      // apply (a record does not break the main stream's PDL chain)
+      CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));
       if (ctx->pl.N > 1)  // N == 1: coal wrote every row to its receive slot directly
         CKC(ctx, run_k(ctx, EMB_K_DEFPUSH, side, [&] { return launch_defpush(c, lc, p, side); }));
       CKC(ctx, gate(ctx, p, GATE_PUB1, 0, side));
@@ -805,7 +837,7 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
     if (ctx->ev_tables[i]) cudaEventDestroy(ctx->ev_tables[i]);
   }
-  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side}) {
+  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre}) {
     if (e) cudaEventDestroy(e);
   }
   delete ctx;

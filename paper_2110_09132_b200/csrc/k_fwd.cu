@@ -84,9 +84,8 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     src_base[v] = (c16 < c.cpr) ? shard_of(c, s) : nullptr;
     src_off[v] = (c16 - s * c.cps) * 16;
   }
-  if (dedup) {
-    // N > 1, prefetched: the sort of this batch is complete (GATE_FWD waited
-    // it), so every distinct row is pulled once per reduce chunk (<= C equal
+  if (dedup && c.fwd_dd[p]) {
+    // N > 1, prefetched, and the sort of this batch was complete at GATE_FWD: every distinct row is pulled once per reduce chunk (<= C equal
     // ids, ascending positions) and stored to all of the chunk's positions —
     // the NVLink bytes of the forward drop from T_r to ~(U_r + Zipf-head chunks)
     // rows (forward dedup).  Dropped keys (pad when

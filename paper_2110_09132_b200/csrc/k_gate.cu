@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         wait_all(c, f->prior_done, t - 1, 1);
         wait_all(c, f->def_done, t - 2, 2);
         if (flag_arg & 1) wait_local(c, c.marked + (p ^ 1), t - 1, 3);  // the prefetch copy this forward checks
-        if (flag_arg & 2) wait_local(c, c.sorted + p, t, 3 * 16 + 1);    // the forward dedups with sort(t)
+        if (flag_arg & 2) c.fwd_dd[p] = ((int)(ld_acquire_gpu(c.sorted + p) - t) >= 0) ? 1u : 0u;  // dedup iff sorted
         EMB_TR_END(10 + kind, t);
         break;
       }
@@ -56,6 +56,11 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // (the scheduled merge reads the merge plan, not the routing tables, so
         // only this rank's scheduled push of tt-2 must be past them)
         if ((flag_arg & 4) && c.mode == SPLIT && tt >= 3) wait_local(c, c.seq + SEQ_DEFPUSHED, tt - 2, 5 * 16);
+        // 8 (SPLIT): the merge plan / D_next tags of parity tt-1 are free once
+        // this rank's scheduled merge of tt-3 is done (the work may start before
+        // the forward of tt-1 when emb_prefetch forked it early)
+        if ((flag_arg & 8) && c.mode == SPLIT && tt >= 4)
+          wait_flag(c, &flags_of(c, c.r)->def_done[c.r], tt - 3, 5 * 16 + 1);
         EMB_TR_END(10 + kind, tt);
         break;
       }

@@ -31,7 +31,7 @@ MODES = {"raw": EMB_BWD_RAW, "coal": EMB_BWD_COAL, "split": EMB_BWD_SPLIT}
 
 EXPORTED = [
     "emb_status_str", "emb_workspace_bytes", "emb_create", "emb_ipc_handle", "emb_get_unique_id",
-    "emb_shard_init", "emb_forward_exchange", "emb_backward_exchange", "dense_allreduce_enqueue",
+    "emb_shard_init", "emb_forward_exchange", "emb_prefetch", "emb_backward_exchange", "dense_allreduce_enqueue",
     "dense_queue_flush", "dense_wait", "emb_flush", "emb_join", "emb_profile", "emb_profile_read",
     "emb_get_stats", "emb_debug_copy", "emb_state_ptr", "emb_queue_issue_order", "emb_shard_destroy",
 ]
@@ -89,6 +89,7 @@ def lib():
             "emb_shard_init": [vp, u8p, u8p, vp, vp],
             "emb_forward_exchange": [vp, vp, i32, vp, vp],
             "emb_backward_exchange": [vp, vp, vp, i32, vp],
+            "emb_prefetch": [vp, vp, i32, vp],
             "dense_allreduce_enqueue": [vp, vp, i64, i32, i32, vp, ctypes.POINTER(i64)],
             "dense_queue_flush": [vp],
             "dense_wait": [vp, i64, vp],
@@ -178,6 +179,10 @@ def emb_shard_init(ctx, peer_handles, nccl_id, shard_init, stream=None):
 def emb_forward_exchange(ctx, ids, out, stream=None):
     _ck(lib().emb_forward_exchange(ctx, _ptr(ids), int(ids.numel()), _ptr(out), _stream(stream)),
         "emb_forward_exchange")
+
+
+def emb_prefetch(ctx, next_ids, stream=None):
+    _ck(lib().emb_prefetch(ctx, _ptr(next_ids), int(next_ids.numel()), _stream(stream)), "emb_prefetch")
 
 
 def emb_backward_exchange(ctx, grad_out, next_ids=None, stream=None):

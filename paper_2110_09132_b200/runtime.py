@@ -61,6 +61,9 @@ class EmbraceExchange:
         E.emb_forward_exchange(self.ctx, ids, out, stream)
         return out
 
+    def prefetch(self, next_ids, stream=None):
+        E.emb_prefetch(self.ctx, next_ids, stream)
+
     def backward(self, grad_out, next_ids=None, stream=None):
         E.emb_backward_exchange(self.ctx, grad_out, next_ids, stream)
 

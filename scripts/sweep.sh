@@ -6,13 +6,13 @@ tag=${1:-sweep}
 out=gpurun_out/$tag
 mkdir -p $out
 ngpu=$(nvidia-smi -L | wc -l)
-python bench.py > $out/default_n1.json 2> $out/default_n1.err
+timeout 300 python bench.py > $out/default_n1.json 2> $out/default_n1.err
 python bench.py --impl reference --steps 3 --warmup 1 > $out/reference_n1.json 2> $out/reference_n1.err
 for cfg in lstm_lm gnmt transformer bert_large; do
-  CUDA_VISIBLE_DEVICES=0 python bench.py --config $cfg --no-cpu-baseline > $out/${cfg}_n1.json 2> $out/${cfg}_n1.err
+  CUDA_VISIBLE_DEVICES=0 EMB_TIMEOUT_MS=2000 timeout 240 python bench.py --config $cfg --no-cpu-baseline > $out/${cfg}_n1.json 2> $out/${cfg}_n1.err
   for n in 2 4 8; do
     [ $n -le $ngpu ] || continue
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+    EMB_TIMEOUT_MS=2000 timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
       --master-port $((29500 + n)) bench.py --gpus $n --config $cfg --no-cpu-baseline > $out/${cfg}_n$n.json 2> $out/${cfg}_n$n.err
   done
 done

@@ -33,7 +33,7 @@ def _np64(t):
 
 
 def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad_id=-1, last_none=True,
-               device=0, rows_sample=None, ids_override=None, check=True, report=None):
+               device=0, rows_sample=None, ids_override=None, check=True, report=None, prefetch=False):
     """Run `iters` iterations on this rank and assert parity after each.
     Returns a dict of max errors seen (for reporting)."""
     import torch
@@ -69,8 +69,11 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
             nxt = None if (last_none and k == iters - 1) else wl.ids[k + 1]
             ids_t = _to_torch(wl.ids[k][rank].astype(np.int32), None, dev)
             dY_t = _to_torch(wl.dY[k][rank], cfg.dtype, dev)
+            nxt_t = None if nxt is None else _to_torch(nxt[rank].astype(np.int32), None, dev)
+            if prefetch and nxt_t is not None:
+                ex.prefetch(nxt_t)  # emb_prefetch: the next batch's work forks before this forward
             Y = ex.forward(ids_t)
-            ex.backward(dY_t, None if nxt is None else _to_torch(nxt[rank].astype(np.int32), None, dev))
+            ex.backward(dY_t, nxt_t)
             ex.flush()
             res = exchange.simulate_iteration(shards, wl.ids[k], wl.dY[k], nxt, t, mode, cfg.dtype, opt, m, v,
                                               pad_id)

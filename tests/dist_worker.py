@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override sequences per rank (0 = config's)")
     ap.add_argument("--pad-id", type=int, default=-1)
     ap.add_argument("--optim", default=None)
+    ap.add_argument("--prefetch", action="store_true", help="call emb_prefetch before every forward")
     args = ap.parse_args()
 
     import torch
@@ -48,7 +49,7 @@ def main():
             cfg, seq_len=args.batch)
     try:
         errs = parity_run(cfg, N=world, rank=rank, mode=args.mode, iters=args.iters, device=local,
-                          pad_id=args.pad_id, optim=args.optim)
+                          pad_id=args.pad_id, optim=args.optim, prefetch=args.prefetch)
         print(f"PARITY OK rank={rank} world={world} config={args.config} mode={args.mode} errs={errs}", flush=True)
         code = 0
     except Exception:

@@ -59,3 +59,12 @@ def test_pad_dropped_multi():
     if _ngpus() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, "--config", "gnmt", "--mode", "split", "--iters", "3", "--batch", "16", "--pad-id", "0")
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_prefetch_multi(n):
+    """emb_prefetch before every forward: the next batch's push / tags / plan /
+    sort fork before the forward; values unchanged."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, "--config", "lstm_lm", "--mode", "split", "--iters", "4", "--batch", "16", "--prefetch")

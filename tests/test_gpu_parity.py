@@ -150,3 +150,11 @@ def test_run_twice_bitwise_deterministic():
         ex.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_prefetch_split_adam():
+    """emb_prefetch (the paper's prefetch as an early fork point) before every forward."""
+    cfg = get_config("tiny")
+    parity_run(cfg, N=1, mode="split", iters=4, optim="adam", lr=1e-3, prefetch=True)
+    parity_run(dataclasses.replace(get_config("lstm_lm"), batch=16), N=1, mode="split", iters=3,
+               rows_sample=512, prefetch=True)
