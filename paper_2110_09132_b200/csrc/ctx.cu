@@ -478,7 +478,12 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   //   point is that earlier position (the next batch's work overlaps forward(t)).
   const bool early = ctx->pf_armed && ctx->pf_ids == next_ids && ctx->pf_n == n_next && next_ids != nullptr;
   ctx->pf_armed = false;
-  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 3;  // debug: 1 aux, 2 side
+  // The early fork is not enabled yet: the aux / side kernels derive the
+  // iteration number from t_rec, which the forward of t writes (a sort forked
+  // before it computed a stale epoch — observed as timeouts).  It needs
+  // per-stream iteration counters first; until then emb_prefetch only records
+  // its position.
+  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 0;
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
   CKC(ctx, cudaStreamWaitEvent(aux, (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p], 0));
   CKC(ctx, cudaStreamWaitEvent(side, (early && (pf_mode & 2)) ? ctx->ev_pre : ctx->ev_main[p], 0));
