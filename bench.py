@@ -152,9 +152,11 @@ def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
     P = np.intersect1d(Uall, nxt).size if mode == "split" else Uall.size
     Q = Uall.size - P
     out = {}
-    # forward: Y write + distinct rows read (every owner's slice) + ids; NVLink in = (N-1)/N of rows
+    # forward: Y write + distinct rows read (every owner's slice) + ids; NVLink in: every distinct row's
+    # N-1 remote slices once (the volume a deduplicating pull must move; the paper's plain AlltoAll
+    # moves (N-1)*T*d*e, reading R10)
     out["fwd_pull_gather"] = (T[rank] * cfg.D * esz + u_fwd * cfg.D * esz + T[rank] * 4,
-                              (N - 1) * T[rank] * d * esz)
+                              (N - 1) * u_fwd * d * esz)
     # a5 prefetch push (+ D_next marks in SPLIT); a6 sort (aux stream); a8 tables (aux)
     out["mark_next"] = (T[rank] * 4 * (N + 1) + (sum(T) * 8 if mode == "split" else 0), (N - 1) * T[rank] * 4)
     out["sort_unique"] = (sum(T) * 4 * 3 + sum(u) * 4 * 4 + (sum(u) * 8 if N > 1 else 0), 0)
