@@ -14,8 +14,11 @@
 #include "../../include/embrace.h"
 #include "common.cuh"
 
+// Rows per sender reduce chunk (B5): shorter chunks mean more warps in flight
+// for the Zipf tail but more partials to combine for the head (the pad id is
+// one huge segment); measured best: 8 up to 8192 tokens per rank, 16 above.
 #ifndef EMB_C
-#define EMB_C 16
+#define EMB_C 0
 #endif
 #include "dense_queue.h"
 #include "kernels.cuh"
@@ -62,7 +65,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   pl->cpr = cfg->dim * pl->esz / 16;
   pl->cps = pl->d * pl->esz / 16;
   if (pl->cpr > 256 || cfg->dim > 1024) return EMB_ERR_SHAPE;  // rows up to 4 KB; fp32 sums of D <= 1024
-  pl->C = EMB_C;  // rows per sender reduce chunk (B5)
+  pl->C = EMB_C > 0 ? EMB_C : (cfg->max_tokens <= 8192 ? 8 : 16);
   pl->max_chunks = cfg->max_tokens + cfg->max_tokens / pl->C + 1;
   pl->max_long = cfg->max_tokens / (pl->C + 1) + 1;
   pl->idbits = bits_for(cfg->vocab);  // the value L itself is the invalid-id sentinel
