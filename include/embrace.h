@@ -204,11 +204,9 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
  * after backward(t-1) and before forward(t) with the ids of iteration t+1
  * (the same device pointer and count later passed to backward(t) as
  * next_ids), once their values are in place in stream order.  The library
- * validates and records this position as the point from which the next
- * batch's prefetch push, sort and D_next tags may start (overlapping
- * forward(t)).  Round 1: the position is recorded but the work still starts
- * at backward(t) (the auxiliary streams need their own iteration counters
- * first, B7).  Calling it or not never changes values.
+ * starts the next batch's prefetch push, sort and D_next tags at this point
+ * (overlapping forward(t)) instead of at backward(t).  Calling it or not
+ * never changes values.
  *   errors: EMB_ERR_STATE if called between a forward and its backward or
  *           twice; EMB_ERR_CAPACITY if n_next > max_tokens.                  */
 emb_status emb_prefetch(emb_ctx* ctx, const int32_t* next_ids, int32_t n_next, emb_stream_t stream);

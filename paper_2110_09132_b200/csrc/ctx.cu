@@ -429,7 +429,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_main[p], 0));
     CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, sq));
     CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
-      return launch_sort(ctx->dc, p, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, sq);
+      return launch_sort(ctx->dc, p, nullptr, 0, 0, ctx->pl.key64, ctx->pl.sort_smem, sq);
     }));
     CKC(ctx, cudaEventRecord(ctx->ev_sorted[p], sq));
     ctx->sort_pending[p] = true;
@@ -481,12 +481,10 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   //   point is that earlier position (the next batch's work overlaps forward(t)).
   const bool early = ctx->pf_armed && ctx->pf_ids == next_ids && ctx->pf_n == n_next && next_ids != nullptr;
   ctx->pf_armed = false;
-  // The early fork is not enabled yet: the aux / side kernels derive the
-  // iteration number from t_rec, which the forward of t writes (a sort forked
-  // before it computed a stale epoch — observed as timeouts).  It needs
-  // per-stream iteration counters first; until then emb_prefetch only records
-  // its position.
-  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 0;
+  // The aux / side kernels of backward(t) take t from sorted[p] (the sort of t
+  // precedes them on their stream), never from t_rec (written by forward(t),
+  // which an early fork may precede).  EMB_PF_MODE (debug): 1 aux, 2 side.
+  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 3;
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
   CKC(ctx, cudaStreamWaitEvent(aux, (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p], 0));
   CKC(ctx, cudaStreamWaitEvent(side, (early && (pf_mode & 2)) ? ctx->ev_pre : ctx->ev_main[p], 0));
@@ -510,7 +508,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     if (next_ids) {
       if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_tables[p ^ 1], 0));
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
-        return launch_sort(c, p ^ 1, next_ids, n_next, ctx->pl.key64, ctx->pl.sort_smem, aux);
+        return launch_sort(c, p ^ 1, next_ids, n_next, 1, ctx->pl.key64, ctx->pl.sort_smem, aux);
       }));
       CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
       ctx->sort_pending[p ^ 1] = true;
@@ -539,13 +537,13 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // scheduled push of t-1 past the routing tables) -> D_next tags -> merge
     // plan -> sort(t+1) -> the Alg. 1 tables of t (presentation, last).
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, aux); }));
-    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4 | 8, aux));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4 | 8 | 16, aux));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, aux); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;
     if (next_ids) {
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
-        return launch_sort(c, p ^ 1, nullptr, 0, ctx->pl.key64, ctx->pl.sort_smem, aux);
+        return launch_sort(c, p ^ 1, nullptr, 0, 1, ctx->pl.key64, ctx->pl.sort_smem, aux);
       }));
       CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
       ctx->sort_pending[p ^ 1] = true;

@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // forward or markpush) pushed this rank's ids: publish them; 2 = wait
         // for every source's ids; 4 (SPLIT) = the routing tables of parity p are
         // free once this rank's scheduled push of tt-2 (side stream) is past.
-        const uint32_t tt = c.t_rec[p ^ 1] + 1;
+        // 16 = launched from a backward (batch t+1): one past the sort of t on
+        // this stream; else from a forward (batch t), after it
+        const uint32_t tt = (flag_arg & 16) ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, tt);
         if (flag_arg & 1) publish(c, EMB_FLAG_OFF(ids), tt);
         if (flag_arg & 2) wait_all(c, flags_of(c, c.r)->ids, tt, 4);

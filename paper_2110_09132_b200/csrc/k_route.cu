@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
                                                              int n_next) {
   EMB_TR_ENTRY();
   pdl_wait();
-  const uint32_t t = c.t_rec[p];
+  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   (void)t;
   EMB_TR_BEGIN(2, t);
   const int s = blockIdx.x % c.N, k = blockIdx.x / c.N;
@@ -119,7 +119,7 @@ static constexpr int MT_CTAS_PER_SRC = 8;
 __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark, int set_flag) {
   EMB_TR_ENTRY();
   pdl_wait();
-  const uint32_t t = c.t_rec[p];
+  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   EMB_TR_BEGIN(17, t);
   if (blockIdx.x == 0 && threadIdx.x < 2) c.plan_cnt[p * 2 + threadIdx.x] = 0;  // re-arm the plan of parity p
   if (do_mark) {
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, in
 __global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
-  const uint32_t t = c.t_rec[p];
+  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   EMB_TR_BEGIN(19, t);
   int cnt[EMB_WMAX];
   int total = 0;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) 
   const int n = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const uint32_t t = c.t_rec[p];
+  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   EMB_TR_BEGIN(9, t);
   const int U = counts_of(c, p, n)[CNT_U];
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;

@@ -78,7 +78,8 @@ __device__ __forceinline__ void cluster_exsum(cg::cluster_group& cluster, int* s
 }
 
 template <typename K, int EPT>
-__global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, const int* own_ids, int own_n) {
+__global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, const int* own_ids, int own_n,
+                                                             int from_bwd) {
   EMB_TR_ENTRY();
   pdl_wait();
   cg::cluster_group cluster = cg::this_cluster();
@@ -98,7 +99,10 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   const unsigned lt = (1u << lane) - 1u;
   const int cr = (int)cluster.block_rank();
   const int n = blockIdx.x / CL;  // source
-  const uint32_t tt = c.t_rec[p ^ 1] + 1;  // iteration of the batch (see sort note in k_route.cu history)
+  // iteration of the batch: from a backward (batch t+1), one past the sort of
+  // t that precedes on this stream — valid even if forward(t) has not run yet
+  // (an early fork); from a forward (batch t, not prefetched), after it.
+  const uint32_t tt = from_bwd ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
   EMB_TR_BEGIN(1, tt);
   // N > 1: the gate before this kernel published / waited the ids flags.
   // own_ids (N == 1 prefetch): this rank's batch is read straight from the caller.
@@ -404,12 +408,12 @@ cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem) {
   return cudaSuccess;
 }
 
-cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
-                        cudaStream_t s) {
+cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, int from_bwd, bool key64,
+                        size_t smem, cudaStream_t s) {
   void* f = key64 ? csort_fn<unsigned long long>(cs_ept(c.max_tok)) : csort_fn<uint32_t>(cs_ept(c.max_tok));
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
-  void* args[] = {&cc, &p, &own_ids, &own_n};
+  void* args[] = {&cc, &p, &own_ids, &own_n, &from_bwd};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c.N * CL);
   cfg.blockDim = dim3(CS_THREADS);

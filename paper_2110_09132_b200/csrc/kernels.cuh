@@ -87,8 +87,8 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
                        int prefetched, int sort_gate, int dedup, cudaStream_t s);
 // a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
 // owner routing (slotmap) — auxiliary stream, one iteration ahead
-cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, bool key64, size_t smem,
-                        cudaStream_t s);
+cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, int from_bwd, bool key64,
+                        size_t smem, cudaStream_t s);
 size_t sort_smem_bytes(int max_tok, bool key64);
 cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
 // a5: prefetch all-gather of the next ids (markpush) and the D_next epoch tags
