@@ -86,6 +86,8 @@ struct DevCtx {
   unsigned int* t_rec;    // [2]   t of the iteration using parity p
   unsigned int* sorted;   // [2]   t of the last completed sort of parity p (gate before the coalesce)
   unsigned int* sort_cnt; // [2]   clusters of the running sort that finished (re-armed by the last)
+  unsigned int* sort_count; // [2] completed sorts of parity p (one per iteration: ceil(t/2) after t)
+  unsigned int* side_it;  // [1]   N == 1: backward calls seen by the side stream (its iteration number)
   unsigned int* marked;   // [2]   t of the last completed mark (prefetch push + D_next tags) of parity p
   unsigned int* mark_cnt; // [2]   CTAs of the running mark that finished (re-armed by the last)
   unsigned int* seq;      // [4]   main-stream progress: [SEQ_BWD] = t past gate_sorted, [SEQ_APPLIED] = t past apply

@@ -112,11 +112,12 @@ struct emb_ctx {
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
+  cudaStream_t aux2 = nullptr;  // N == 1: the sorts of odd batches (two sorts may overlap; 8 SMs each)
   cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
   bool tables_pending[2] = {false, false};  // N == 1: tables(t) on the side stream still reads parity t&1
-  cudaEvent_t ev_marked = nullptr, ev_join_aux = nullptr, ev_join_side = nullptr;
+  cudaEvent_t ev_marked = nullptr, ev_join_aux = nullptr, ev_join_side = nullptr, ev_join_aux2 = nullptr;
   bool mark_pending = false;  // N == 1: mark runs on the side stream; the next forward checks its pushed ids
   bool aux_used = false, side_used = false;  // since the last emb_join
   long long it = 0;          // forward calls so far (host mirror of the device t)
@@ -277,6 +278,8 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.t_rec, 2 * 4);
     ALLOC(c.sorted, 2 * 4);
     ALLOC(c.sort_cnt, 2 * 4);
+    ALLOC(c.sort_count, 2 * 4);
+    ALLOC(c.side_it, 4);
     ALLOC(c.marked, 2 * 4);
     ALLOC(c.mark_cnt, 2 * 4);
     ALLOC(c.seq, 4 * 4);
@@ -300,6 +303,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
     if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo) != cudaSuccess) goto fail;
     if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
+    if (cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
   }
   for (int i = 0; i < 2; ++i) {
     if (cudaEventCreateWithFlags(&ctx->ev_prior[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
@@ -311,6 +315,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   if (cudaEventCreateWithFlags(&ctx->ev_marked, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_aux, cudaEventDisableTiming) != cudaSuccess) goto fail;
+  if (cudaEventCreateWithFlags(&ctx->ev_join_aux2, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_side, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
   *out = ctx;
@@ -425,7 +430,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
-    cudaStream_t sq = ctx->aux;
+    cudaStream_t sq = (ctx->pl.N == 1 && (p & 1)) ? ctx->aux2 : ctx->aux;
     CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_main[p], 0));
     CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, sq));
     CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
@@ -486,7 +491,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // which an early fork may precede).  EMB_PF_MODE (debug): 1 aux, 2 side.
   static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 3;
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
-  CKC(ctx, cudaStreamWaitEvent(aux, (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p], 0));
+  cudaEvent_t fork = (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p];
+  CKC(ctx, cudaStreamWaitEvent(aux, fork, 0));
   CKC(ctx, cudaStreamWaitEvent(side, (early && (pf_mode & 2)) ? ctx->ev_pre : ctx->ev_main[p], 0));
   ctx->aux_used = ctx->side_used = true;
   // the sort of this batch (aux stream) must be complete: a one-warp gate on a
@@ -506,11 +512,15 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     //         the a8 slot tables of this batch.
     // next_ids is read asynchronously until the next backward (header contract).
     if (next_ids) {
-      if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_tables[p ^ 1], 0));
-      CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
-        return launch_sort(c, p ^ 1, next_ids, n_next, 1, ctx->pl.key64, ctx->pl.sort_smem, aux);
+      // the sort of t+1 goes to the stream of its parity: consecutive sorts may
+      // overlap (each is one 8-SM cluster), so the sort no longer bounds the step
+      cudaStream_t sq = ((p ^ 1) & 1) ? ctx->aux2 : aux;
+      CKC(ctx, cudaStreamWaitEvent(sq, fork, 0));
+      if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_tables[p ^ 1], 0));
+      CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
+        return launch_sort(c, p ^ 1, next_ids, n_next, 2, ctx->pl.key64, ctx->pl.sort_smem, sq);
       }));
-      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], sq));
       ctx->sort_pending[p ^ 1] = true;
       ctx->tables_pending[p ^ 1] = false;
     }
@@ -519,11 +529,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // spinning side gate started before the forward was observed to hold back
     // the main stream's launches — timeouts)
     if (ctx->sort_pending[p]) CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_sorted[p], 0));
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_markpush(c, p, next_ids, n_next, side); }));
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, 1, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_markpush(c, p, next_ids, n_next, 1, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, side, [&] { return launch_marktag(c, p, do_mark, 1, 1, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_marked, side));
     ctx->mark_pending = true;
-    CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, side); }));
+    CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, 1, side); }));
     CKC(ctx, cudaEventRecord(ctx->ev_tables[p], side));
     ctx->tables_pending[p] = true;
     ctx->side_used = true;
@@ -536,9 +546,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // push ids(t+1) -> one gate (publish + wait ids(t+1), and this rank's
     // scheduled push of t-1 past the routing tables) -> D_next tags -> merge
     // plan -> sort(t+1) -> the Alg. 1 tables of t (presentation, last).
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, aux); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, 0, aux); }));
     CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4 | 8 | 16, aux));
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, aux); }));
+    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, 0, aux); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;
     if (next_ids) {
@@ -548,7 +558,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
       ctx->sort_pending[p ^ 1] = true;
     }
-    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, aux); }));
+    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, 0, aux); }));
   }
   ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
@@ -652,6 +662,10 @@ emb_status emb_join(emb_ctx* ctx, emb_stream_t stream_) {
   if (ctx->aux_used) {
     CKC(ctx, cudaEventRecord(ctx->ev_join_aux, ctx->aux));
     CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux, 0));
+    if (ctx->pl.N == 1) {
+      CKC(ctx, cudaEventRecord(ctx->ev_join_aux2, ctx->aux2));
+      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux2, 0));
+    }
     ctx->aux_used = false;
   }
   if (ctx->side_used) {
@@ -836,6 +850,7 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
   if (ctx->sym) cudaFree(ctx->sym);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
   for (int i = 0; i < 2; ++i) {
     if (ctx->ev_prior[i]) cudaEventDestroy(ctx->ev_prior[i]);
     if (ctx->ev_def[i]) cudaEventDestroy(ctx->ev_def[i]);
@@ -843,7 +858,7 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
     if (ctx->ev_tables[i]) cudaEventDestroy(ctx->ev_tables[i]);
   }
-  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre}) {
+  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre, ctx->ev_join_aux2}) {
     if (e) cudaEventDestroy(e);
   }
   delete ctx;

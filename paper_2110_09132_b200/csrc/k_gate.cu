@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // N == 1 also the prefetch check (fingerprints of fwd(t) and sort(t))
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
-        wait_local(c, c.sorted + p, t, 9 * 16);
+        wait_local(c, c.sort_count + p, (t + 1) / 2, 9 * 16);  // one sort of parity p per iteration
         unsigned* f = c.fp + p * 4;
         if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
         f[0] = f[1] = f[2] = f[3] = 0;

@@ -82,10 +82,13 @@ static constexpr int MP_SLICES = 4;   // CTAs per destination
 static constexpr int MP_THREADS = 256;
 static constexpr int MK = 8;          // ids in flight per thread
 __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, const int* __restrict__ next_ids,
-                                                             int n_next) {
+                                                             int n_next, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
-  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
+  // t of this batch: N > 1 the sort of t precedes on this stream (DESIGN B7);
+  // N == 1 (side stream) the side stream's own count of backward calls
+  if (t_mode && blockIdx.x == 0 && threadIdx.x == 0) c.side_it[0] += 1;
+  const uint32_t t = t_mode ? c.side_it[0] + 1 : __ldcg(c.sorted + p);
   (void)t;
   EMB_TR_BEGIN(2, t);
   const int s = blockIdx.x % c.N, k = blockIdx.x / c.N;
@@ -116,10 +119,10 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
 // ids flags), tag D_next: nextmark[p][id] = t+1 (epoch tag, never cleared), so
 // the split is a per-id test everywhere.  Then the completion flag marked[p].
 static constexpr int MT_CTAS_PER_SRC = 8;
-__global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark, int set_flag) {
+__global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark, int set_flag, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
-  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
+  const uint32_t t = t_mode ? __ldcg(c.side_it) : __ldcg(c.sorted + p);  // see markpush
   EMB_TR_BEGIN(17, t);
   if (blockIdx.x == 0 && threadIdx.x < 2) c.plan_cnt[p * 2 + threadIdx.x] = 0;  // re-arm the plan of parity p
   if (do_mark) {
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
 // Slot order of the paper's presentation: P_n = U_n ∩ D_next ascending, then
 // D_n = U_n \ P_n ascending (a stable ballot partition of the unique ids).
 template <int EPT>
-__global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) {
+__global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
   __shared__ int s_tmp[64];
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p) 
   const int n = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
+  const uint32_t t = t_mode ? __ldcg(c.side_it) : __ldcg(c.sorted + p);  // see markpush
   EMB_TR_BEGIN(9, t);
   const int U = counts_of(c, p, n)[CNT_U];
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
@@ -294,12 +297,13 @@ static void* tables_fn(int ept) {
   return nullptr;
 }
 
-cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, cudaStream_t s) {
-  return launch_pdl(markpush_kernel, dim3(c.N * MP_SLICES), dim3(MP_THREADS), 0, s, c, p, next_ids, n_next);
+cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, int t_mode, cudaStream_t s) {
+  return launch_pdl(markpush_kernel, dim3(c.N * MP_SLICES), dim3(MP_THREADS), 0, s, c, p, next_ids, n_next, t_mode);
 }
 
-cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, cudaStream_t s) {
-  return launch_pdl(marktag_kernel, dim3(c.N * MT_CTAS_PER_SRC), dim3(MP_THREADS), 0, s, c, p, do_mark, set_flag);
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, int t_mode, cudaStream_t s) {
+  return launch_pdl(marktag_kernel, dim3(c.N * MT_CTAS_PER_SRC), dim3(MP_THREADS), 0, s, c, p, do_mark, set_flag,
+                    t_mode);
 }
 
 cudaError_t launch_plan(const DevCtx& c, int p, cudaStream_t s) {
@@ -309,11 +313,11 @@ cudaError_t launch_plan(const DevCtx& c, int p, cudaStream_t s) {
   return launch_pdl(plan_kernel, dim3(grid), dim3(MP_THREADS), 0, s, c, p);
 }
 
-cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s) {
+cudaError_t launch_tables(const DevCtx& c, int p, int t_mode, cudaStream_t s) {
   void* f = tables_fn(ept_for(c.max_tok));
   if (!f) return cudaErrorInvalidValue;
   DevCtx cc = c;
-  void* args[] = {&cc, &p};
+  void* args[] = {&cc, &p, &t_mode};
   return launch_pdl_raw(f, dim3(c.N), dim3(RT_THREADS), 0, s, args);
 }
 

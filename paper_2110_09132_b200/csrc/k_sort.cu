@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   // iteration of the batch: from a backward (batch t+1), one past the sort of
   // t that precedes on this stream — valid even if forward(t) has not run yet
   // (an early fork); from a forward (batch t, not prefetched), after it.
-  const uint32_t tt = from_bwd ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
+  // (from_bwd == 2, N == 1: the sorts of consecutive batches run on two
+  // streams and may overlap; only the completion count is published, the
+  // epoch is not needed — no slotmap at N == 1)
+  const uint32_t tt = from_bwd == 2 ? 0u : from_bwd ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
   EMB_TR_BEGIN(1, tt);
   // N > 1: the gate before this kernel published / waited the ids flags.
   // own_ids (N == 1 prefetch): this rank's batch is read straight from the caller.
@@ -366,7 +369,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     if (atomicAdd(&c.sort_cnt[p], 1u) == (unsigned)c.N - 1) {
       c.sort_cnt[p] = 0;
       __threadfence();
-      st_release_gpu(&c.sorted[p], tt);
+      if (from_bwd != 2) st_release_gpu(&c.sorted[p], tt);
+      atomicAdd(&c.sort_count[p], 1u);  // after the fence: GATE_SORTED waits the count
     }
   }
   EMB_TR_END(1, tt);

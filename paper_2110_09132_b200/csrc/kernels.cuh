@@ -93,13 +93,13 @@ size_t sort_smem_bytes(int max_tok, bool key64);
 cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem);
 // a5: prefetch all-gather of the next ids (markpush) and the D_next epoch tags
 // (marktag, + completion flag marked[p]) — Alg. 1 line 4's set
-cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, cudaStream_t s);
-cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, cudaStream_t s);
+cudaError_t launch_markpush(const DevCtx& c, int p, const int* next_ids, int n_next, int t_mode, cudaStream_t s);
+cudaError_t launch_marktag(const DevCtx& c, int p, int do_mark, int set_flag, int t_mode, cudaStream_t s);
 // N > 1, after marktag: the owner merge plan of both parts (leaders, sources'
 // unique indices), then the completion flag marked[p]
 cudaError_t launch_plan(const DevCtx& c, int p, cudaStream_t s);
 // a8 presentation: Alg. 1 slot tables P_n ++ D_n, counts p_n (stats / debug; off the critical path)
-cudaError_t launch_tables(const DevCtx& c, int p, cudaStream_t s);
+cudaError_t launch_tables(const DevCtx& c, int p, int t_mode, cudaStream_t s);
 // a7 + a9 (+a10 for the prior part): sender coalesce — segmented reduce in
 // fp32, long (Zipf-head) segments combined by the last-arriving CTA; N == 1
 // applies the optimizer directly, N > 1 pushes prior rows to the owners and
