@@ -413,19 +413,20 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // N > 1 and prefetched: GATE_FWD also waits for sort(t) (computed one
   // iteration ahead), and the forward pulls each distinct row once (dedup)
   // using the sort's chunk descriptors; the coalesce then needs no sort gate.
-  // N == 1: the step is bounded by fwd(t) + sort(t+1) (sort(t+1) is forked
-  // after the forward), so the forward must not wait for the sort there
-  // (sort_gate = 1, CTA 0 waiting at the forward's end, measured slower).
   //   The gate does not wait for sort(t): it only records whether sort(t) is
   //   already complete (fwd_dd[p]); the forward dedups if so, else it gathers
   //   every token (identical Y).  Waiting would put the aux chain (push, tags,
   //   plan, sort) on the critical path when the sort is the slower side (LM).
+  // (sort_gate = 1 — the forward's CTA 0 waiting for the sort's completion
+  // count at its end instead of a gate kernel — measured: GNMT -0.8 us, LM
+  // +2.9 us at N == 1; a CTA spinning in a wide kernel delays other streams'
+  // launches, see §6 Liveness.  Kept off.)
   const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
   const int sort_gate = 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
                  [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, dedup, stream); }));
-  ctx->fwd_sort_gated = false;
+  ctx->fwd_sort_gated = sort_gate != 0;
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)

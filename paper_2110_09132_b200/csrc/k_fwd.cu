@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     // iteration ahead): CTA 0 waits for it here instead of a gate kernel
     // between the two (one kernel boundary less on the main stream), then
     // lets the side stream start this iteration's backward work
-    wait_local(c, c.sorted + p, t, 9 * 16 + 1);
+    wait_local(c, c.sort_count + p, (t + 1) / 2, 9 * 16 + 1);  // one sort of parity p per iteration
     st_release_gpu(c.seq + SEQ_BWD, t);
   }
   EMB_TR_END(0, t);
