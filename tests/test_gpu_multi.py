@@ -48,10 +48,14 @@ def test_tiny_multi(n, mode):
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
-@pytest.mark.parametrize("name", ["lstm_lm", "bert_large"])
+@pytest.mark.parametrize("name", ["lstm_lm", "bert_large", "gnmt"])
 def test_paper_shapes_multi(n, name):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
+    if name == "lstm_lm" and n == 8:
+        # every rank's fp64 oracle holds the 793,470 x 512 table and both Adam
+        # moments (~10 GB per process); N = 8 is covered by BERT / GNMT shapes
+        pytest.skip("LM oracle at N = 8: host memory / time; N = 8 covered by bert_large and gnmt")
     _run(n, "--config", name, "--mode", "split", "--iters", "2", "--batch", "16")
 
 
