@@ -90,8 +90,8 @@ struct DevCtx {
   unsigned int* side_it;  // [1]   N == 1: backward calls seen by the side stream (its iteration number)
   unsigned int* marked;   // [2]   t of the last completed mark (prefetch push + D_next tags) of parity p
   unsigned int* mark_cnt; // [2]   CTAs of the running mark that finished (re-armed by the last)
-  unsigned int* seq;      // [4]   main-stream progress: [SEQ_BWD] = t past gate_sorted, [SEQ_APPLIED] = t past apply
-  unsigned int* seen;     // [4]   per waiting stream: how many of those steps it has consumed
+  unsigned int* seq;      // [4]   progress records: [SEQ_BWD] t past the sort gate, [SEQ_APPLIED] t past the
+                          //       apply, [SEQ_DEFPUSHED] t past the scheduled push (the sort of t+2 waits it)
   unsigned int* fwd_dd;   // [2]   N > 1: the forward of parity p dedups (sort(t) was already complete at its gate)
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)

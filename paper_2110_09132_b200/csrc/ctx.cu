@@ -283,7 +283,6 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.marked, 2 * 4);
     ALLOC(c.mark_cnt, 2 * 4);
     ALLOC(c.seq, 4 * 4);
-    ALLOC(c.seen, 4 * 4);
     ALLOC(c.fwd_dd, 2 * 4);
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
@@ -488,13 +487,12 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   const bool early = ctx->pf_armed && ctx->pf_ids == next_ids && ctx->pf_n == n_next && next_ids != nullptr;
   ctx->pf_armed = false;
   // The aux / side kernels of backward(t) take t from sorted[p] (the sort of t
-  // precedes them on their stream), never from t_rec (written by forward(t),
-  // which an early fork may precede).  EMB_PF_MODE (debug): 1 aux, 2 side.
-  static const int pf_mode = getenv("EMB_PF_MODE") ? atoi(getenv("EMB_PF_MODE")) : 3;
+  // precedes them on their stream) or the side stream's own count, never from
+  // t_rec (written by forward(t), which an early fork may precede).
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
-  cudaEvent_t fork = (early && (pf_mode & 1)) ? ctx->ev_pre : ctx->ev_main[p];
+  cudaEvent_t fork = early ? ctx->ev_pre : ctx->ev_main[p];
   CKC(ctx, cudaStreamWaitEvent(aux, fork, 0));
-  CKC(ctx, cudaStreamWaitEvent(side, (early && (pf_mode & 2)) ? ctx->ev_pre : ctx->ev_main[p], 0));
+  CKC(ctx, cudaStreamWaitEvent(side, fork, 0));
   ctx->aux_used = ctx->side_used = true;
   // the sort of this batch (aux stream) must be complete: a one-warp gate on a
   // device flag the sort sets (a host event here would break the PDL chain);

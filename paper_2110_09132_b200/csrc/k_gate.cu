@@ -113,17 +113,6 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         EMB_TR_END(10 + kind, t);
         break;
       }
-      case GATE_SEQ: {
-        // the next main-stream step of kind `si` (host events would break the
-        // main stream's programmatic-launch chain)
-        const int si = flag_arg >> 8, wi = flag_arg & 255;
-        const uint32_t target = c.seen[wi] + 1;
-        EMB_TR_BEGIN(18, target);
-        wait_local(c, c.seq + si, target, 10 * 16 + si * 4 + wi);
-        c.seen[wi] = target;
-        EMB_TR_END(18, target);
-        break;
-      }
       default:
         atomicOr(c.err, ERR_STATE);
     }

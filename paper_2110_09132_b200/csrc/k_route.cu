@@ -28,33 +28,6 @@ namespace emb {
 static constexpr int RT_THREADS = 1024;
 static constexpr int RT_WARPS = RT_THREADS / 32;
 
-// Block-wide exclusive scan of one int per thread; *total receives the sum.
-__device__ __forceinline__ int block_exscan(int v, int* tmp, int* total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) tmp[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int s = (lane < RT_WARPS) ? tmp[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    tmp[lane] = s;
-  }
-  __syncthreads();
-  const int before = (w > 0) ? tmp[w - 1] : 0;
-  *total = tmp[RT_WARPS - 1];
-  __syncthreads();
-  return before + x - v;
-}
-
 // Two-counter exclusive scan of per-warp totals wa[32], wb[32] (warp 0 does
 // it); results back in place, grand totals in tot[0..1].
 __device__ __forceinline__ void warp_totals_scan(int* wa, int* wb, int* tot) {

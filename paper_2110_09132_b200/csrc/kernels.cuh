@@ -74,11 +74,10 @@ enum GateKind {
   GATE_PUB1 = 3,     // side, before merge(part 1)
   GATE_SORTED = 4,   // main, before the coalesce: sort(t) done (+ N == 1 prefetch check)
   GATE_MARKED = 5,   // main, before the apply (SPLIT): D_next tags of t+1 done
-  GATE_DEFDONE = 6,  // side, after merge(part 1): publish def_done(t) to every owner
-  GATE_SEQ = 7       // aux / side: wait for the next main-stream step (flag_arg = seq << 8 | waiter)
+  GATE_DEFDONE = 6   // side, after merge(part 1): publish def_done(t) to every owner
 };
+// main / side-stream progress records (device flags, epoch t)
 enum SeqIndex { SEQ_BWD = 0, SEQ_APPLIED = 1, SEQ_DEFPUSHED = 2 };
-enum SeqWaiter { W_AUX = 0, W_SIDE = 1 };
 cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStream_t s);
 
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
