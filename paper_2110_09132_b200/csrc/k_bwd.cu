@@ -322,6 +322,13 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
   pdl_trigger();
 }
 
+#ifndef EMB_APPLY_EA_F32
+#define EMB_APPLY_EA_F32 2
+#endif
+#ifndef EMB_APPLY_EA_BF16
+#define EMB_APPLY_EA_BF16 1
+#endif
+#define EMB_APPLY_EA(EPV) ((EPV) == 4 ? EMB_APPLY_EA_F32 : EMB_APPLY_EA_BF16)  // single-chunk rows in flight per thread
 #ifndef EMB_APPLY_MINB
 #define EMB_APPLY_MINB 4  // measured: 3 -> 4 resident CTAs per SM, LM N=1 23.3 -> 22.0 us
 #endif
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
 
   // (2) single-chunk uniques: RPB rows per CTA pass, thread = one 16-byte wire
   //     chunk (the (row, chunk) split is computed once: no division in the loop)
-  constexpr int EA = (EPV == 4) ? 2 : 1;  // rows in flight per thread
+  constexpr int EA = EMB_APPLY_EA(EPV);  // rows in flight per thread
   const int RPB = BWD_THREADS / c.cpr;
   const int rl = threadIdx.x / c.cpr, c16 = threadIdx.x - rl * c.cpr;
   if (rl < RPB) {
@@ -732,7 +739,7 @@ static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char
 
 template <int DT>
 static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
-  constexpr int EA = (Vec<DT>::EPV == 4) ? 2 : 1;
+  constexpr int EA = EMB_APPLY_EA(Vec<DT>::EPV);
   const int rpb = BWD_THREADS / c.cpr;
   long long grid = ((long long)c.max_tok + (long long)rpb * EA - 1) / ((long long)rpb * EA);
   if (grid > L.nsm * 8) grid = L.nsm * 8;
