@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=64)
+    ap.add_argument("--dense-queue", type=int, default=0, metavar="W",
+                    help="measure the a13 dense AllReduce priority queue with window W (separate JSON line)")
     return ap.parse_args()
 
 
@@ -272,6 +274,136 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- a13 dense queue (separate measurement)
+def run_dense(args, cfg, world, rank, local):
+    """the dense queue is measured separately and in a concurrent
+    run for interference; it is not part of the headline.  Per iteration every
+    rank enqueues the config's dense blocks in BP order (last layer first) with
+    priority = FP order (block 0 = first layer = most urgent),
+    window W (reading R16), then flushes.  Three timed phases (CUDA events on
+    the launching stream, max over ranks): queue alone, sparse step alone
+    (eager), both concurrently (the queue's comm stream overlaps the next
+    iterations' sparse exchange)."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2110_09132_b200 import embrace as E
+    from paper_2110_09132_b200.runtime import EmbraceExchange
+    from synthetic.workloads import gen_dense
+
+    nblk = cfg.dense_blocks or 16
+    nel = cfg.dense_block_elems or 8_400_000
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    blocks = [torch.from_numpy(gen_dense(cfg, k, rank, 1 << 16)).to(tdt).to(dev).repeat((nel >> 16) + 1)[:nel]
+              .contiguous() for k in range(nblk)]
+    nb = n_batches(cfg, world)
+    ids, ids_all, dY = make_batches(cfg, world, rank, nb)
+    ids_d = [torch.from_numpy(x).to(dev) for x in ids]
+    dY_d = [torch.from_numpy(x).to(dev).to(tdt) for x in dY]
+    Y_d = [torch.empty((len(x), cfg.D), dtype=tdt, device=dev) for x in ids]
+    d = cfg.D // world
+    W = gen_table(cfg)
+    shard0 = torch.from_numpy(np.ascontiguousarray(W[:, rank * d:(rank + 1) * d])).to(dev).to(tdt)
+    del W
+    ex = EmbraceExchange(cfg.L, cfg.D, shard0, world=world, rank=rank, device=local, dtype=cfg.dtype,
+                         max_tokens=cfg.max_tokens, mode=args.mode, optim=cfg.optim, lr=cfg.lr,
+                         dense_queue=True, queue_window=args.dense_queue)
+    stream = torch.cuda.current_stream()
+    ready = torch.cuda.Event()
+    prios = list(range(nblk))[::-1]          # enqueued in BP order: the last layer (largest FP index) first
+    last = []
+
+    def sparse(k):
+        b = k % nb
+        E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], stream)
+        E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], stream)
+        E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], stream)
+
+    def dense():
+        ready.record(stream)                 # the blocks' BP is done (stand-in: everything so far on `stream`)
+        tk = [E.dense_allreduce_enqueue(ex.ctx, blocks[p], p, ready) for p in prios]
+        E.dense_queue_flush(ex.ctx)          # issued before `ready` is re-recorded (borrowed event)
+        last[:] = tk
+
+    def timed(fn, K):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        last.clear()
+        fn(K)
+        E.emb_join(ex.ctx, stream)           # deferred sparse parts
+        for tk in last:                      # the queue's comm stream (in-order: the last iteration suffices)
+            E.dense_wait(ex.ctx, tk, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
+
+    def q_only(K):
+        for _ in range(K):
+            dense()
+
+    def s_only(K):
+        for j in range(K):
+            sparse(j)
+
+    def both(K):
+        for j in range(K):
+            sparse(j)
+            dense()
+
+    K = max(3, min(args.steps, 50))
+    for fn in (q_only, s_only, both):       # warm-up (NCCL communicator, kernels)
+        timed(fn, max(3, args.warmup // 4))
+    with ClockSampler(local) as clk:
+        t_q = timed(q_only, K)
+        t_s = timed(s_only, K)
+        t_b = timed(both, K)
+    log = [int(x) for x in ex.debug(E.EMB_DBG_ISSUE_LOG)]
+    want1 = [int(x) for x in E.emb_queue_issue_order(prios, args.dense_queue)]
+    per_iter = [x % nblk for x in log[:nblk]]
+    order_ok = per_iter == want1
+    bytes_blk = nel * (2 if cfg.dtype == "bf16" else 4)
+    tot = nblk * bytes_blk
+    busbw = (2 * (world - 1) / world * tot) / (t_q / K * 1e-3) / 1e9 if world > 1 else 0.0
+    algbw = tot / (t_q / K * 1e-3) / 1e9
+    nvl_peak = 770.0
+    ex.flush()
+    if rank == 0:
+        line = {"metric": "dense AllReduce priority queue (a13): bus GB/s per rank", "value": round(busbw, 1),
+                "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": max(3, args.warmup // 4),
+                "ms_per_step": t_q / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": cfg.dtype, "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: {nblk} dense blocks x {nel} {cfg.dtype} per rank "
+                                       f"({tot / 2**20:.0f} MiB), priority = FP order, enqueued in BP order",
+                           "window": args.dense_queue, "sparse_mode": args.mode},
+                "algbw_gbs": round(algbw, 1),
+                "roofline": {"bound": "nvlink", "achieved": round(busbw, 1), "peak": nvl_peak, "unit": "GB/s",
+                             "frac": round(busbw / nvl_peak, 4) if world > 1 else None,
+                             "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction; ring "
+                                            "bus bytes 2(N-1)/N x buffer (NVLS may exceed it)"},
+                "issue_order": {"first_iteration": per_iter, "rule": want1, "ok": order_ok},
+                "interference": {"queue_ms": t_q / K, "sparse_ms": t_s / K, "both_ms": t_b / K,
+                                 "overlap_frac": round((t_q + t_s - t_b) / min(t_q, t_s), 4)
+                                 if min(t_q, t_s) > 0 else None,
+                                 "note": "sparse steps eager (no graph); overlap_frac 1 = the shorter phase "
+                                         "is fully hidden"},
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -281,6 +413,8 @@ def main():
     cfg = get_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
+    if args.dense_queue:
+        return run_dense(args, cfg, world, rank, local)
 
     import torch
     torch.cuda.set_device(local)

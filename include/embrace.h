@@ -217,7 +217,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
 /* a13: dense-gradient AllReduce priority queue.
  *   buf      : device [count] (fp32 or bf16), averaged in place over ranks
  *   priority : lower = sooner (dense blocks in FP order; reading R16)
- *   ready    : event the producer recorded after this block's backward, or NULL
+ *   ready    : event the producer recorded after this block's backward, or NULL;
+ *              borrowed: it must stay valid and must not be re-recorded until
+ *              the request is issued (the comm stream waits on it at issue time)
  *   ticket   : out, id for dense_wait
  * Issue rule (identical on every rank, a pure function of the enqueue
  * sequence): after each enqueue, while >= W requests are pending, issue the

@@ -74,3 +74,18 @@ def test_prefetch_multi(n):
     if n == 8:
         pytest.skip("tiny: D=16 fp32 at N=8 gives 8-byte column slices (EMB_ERR_SHAPE by design)")
     _run(n, "--config", "tiny", "--mode", "split", "--iters", "4", "--prefetch")
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("window", [1, 3, 7])
+def test_dense_queue_multi(n, window):
+    """a13: dense AllReduce (mean) values vs the oracle, issue order vs the
+    window rule (reading R16), mixed fp32 / bf16 blocks."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "tests", "dense_worker.py"), "--window", str(window)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and out.count("DENSE OK") == n, out[-6000:]
