@@ -329,6 +329,9 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
 #define EMB_APPLY_EA_BF16 1
 #endif
 #define EMB_APPLY_EA(EPV) ((EPV) == 4 ? EMB_APPLY_EA_F32 : EMB_APPLY_EA_BF16)  // single-chunk rows in flight per thread
+#ifndef EMB_APPLY_GRID_PER_SM
+#define EMB_APPLY_GRID_PER_SM 8  // grid cap (the grid is sized from max_tok: U lives on the device)
+#endif
 #ifndef EMB_APPLY_MINB
 #define EMB_APPLY_MINB 4  // measured: 3 -> 4 resident CTAs per SM, LM N=1 23.3 -> 22.0 us
 #endif
@@ -742,7 +745,7 @@ static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cu
   constexpr int EA = EMB_APPLY_EA(Vec<DT>::EPV);
   const int rpb = BWD_THREADS / c.cpr;
   long long grid = ((long long)c.max_tok + (long long)rpb * EA - 1) / ((long long)rpb * EA);
-  if (grid > L.nsm * 8) grid = L.nsm * 8;
+  if (grid > L.nsm * EMB_APPLY_GRID_PER_SM) grid = L.nsm * EMB_APPLY_GRID_PER_SM;
   if (grid < 1) grid = 1;
   return launch_pdl(coal_apply_kernel<DT>, dim3((int)grid), dim3(BWD_THREADS), 0, s, c, p);
 }
