@@ -583,28 +583,69 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # the next-ids buffer of step k is the ids buffer of step k+1 (prefetch contract)
-    ids_buf = [torch.empty(cfg.max_tokens, dtype=torch.int32, device=dev) for _ in range(3)]
-    dY_buf = torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev)
-    Y_buf = torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev)
+    # Three-stage pipeline: H2D of step j+1 (copy stream) and D2H of step j
+    # (second copy stream) overlap the compute on `stream` and each other
+    # (PCIe is full duplex).  Buffer reuse follows embrace.h's borrow rule: a
+    # buffer borrowed at step t may be rewritten once `stream` has passed
+    # backward(t+1) (event done[t+1]).  ids of step j live in ids_buf[j % 4]
+    # (borrowed at j-1 as next_ids and at j as ids), dY in dY_buf[j % 3], Y in
+    # Y_buf[j % 3] (read back by the D2H stream).
+    NI, NB = 4, 3
+    ids_buf = [torch.empty(cfg.max_tokens, dtype=torch.int32, device=dev) for _ in range(NI)]
+    dY_buf = [torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev) for _ in range(NB)]
+    Y_buf = [torch.empty((cfg.max_tokens, cfg.D), dtype=tdt, device=dev) for _ in range(NB)]
+    s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    in_ready, done, out_done = {}, {}, {}
     e0.record(stream)
+    s_h2d.wait_event(e0)
+    s_d2h.wait_event(e0)
+
+    def stage_in(j):
+        # ids(j+1) (and ids(0) at j = 0) plus dY(j)
+        b, bn = (kk + j) % nb, (kk + j + 1) % nb
+        nonlocal_h2d = 0
+        with torch.cuda.stream(s_h2d):
+            if j - 2 in done:
+                # dY_buf[j % 3] and ids_buf[(j+1) % 4] were last borrowed at step j-3
+                s_h2d.wait_event(done[j - 2])
+            if j == 0:
+                ids_buf[0][:h_ids[b].numel()].copy_(h_ids[b], non_blocking=True)
+                nonlocal_h2d += h_ids[b].numel() * 4
+            ids_buf[(j + 1) % NI][:h_ids[bn].numel()].copy_(h_ids[bn], non_blocking=True)
+            dY_buf[j % NB][:h_dY[b].shape[0]].copy_(h_dY[b], non_blocking=True)
+            nonlocal_h2d += h_ids[bn].numel() * 4 + h_dY[b].numel() * h_dY[b].element_size()
+            in_ready[j] = ev()
+            in_ready[j].record(s_h2d)
+        return nonlocal_h2d
+
+    h2d += stage_in(0)
     for j in range(Ke):
-        b = (kk + j) % nb
-        bn = (b + 1) % nb
+        b, bn = (kk + j) % nb, (kk + j + 1) % nb
         n, nn = h_ids[b].numel(), h_ids[bn].numel()
-        cur, nxt = ids_buf[j % 3][:n], ids_buf[(j + 1) % 3][:nn]
-        if j == 0:
-            cur.copy_(h_ids[b], non_blocking=True)
-            h2d += n * 4
-        nxt.copy_(h_ids[bn], non_blocking=True)
-        dY_buf[:n].copy_(h_dY[b], non_blocking=True)
-        h2d += nn * 4 + h_dY[b].numel() * h_dY[b].element_size()
+        cur, nxt = ids_buf[j % NI][:n], ids_buf[(j + 1) % NI][:nn]
+        stream.wait_event(in_ready[j])
+        if j - NB in out_done:
+            stream.wait_event(out_done[j - NB])  # Y_buf[j % 3] read back
+        yb = Y_buf[j % NB]
         E.emb_prefetch(ex.ctx, nxt, stream)
-        E.emb_forward_exchange(ex.ctx, cur, Y_buf[:n], stream)
-        E.emb_backward_exchange(ex.ctx, dY_buf[:n], nxt, stream)
-        h_Y[b].copy_(Y_buf[:n], non_blocking=True)
+        E.emb_forward_exchange(ex.ctx, cur, yb[:n], stream)
+        fwd_done = ev()
+        fwd_done.record(stream)
+        E.emb_backward_exchange(ex.ctx, dY_buf[j % NB][:n], nxt, stream)
+        done[j] = ev()
+        done[j].record(stream)
+        if j + 1 < Ke:
+            h2d += stage_in(j + 1)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(fwd_done)
+            h_Y[b].copy_(yb[:n], non_blocking=True)
+            out_done[j] = ev()
+            out_done[j].record(s_d2h)
         d2h += h_Y[b].numel() * h_Y[b].element_size()
     E.emb_join(ex.ctx, stream)
+    stream.wait_stream(s_d2h)
+    stream.wait_stream(s_h2d)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -640,7 +681,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / Ke), "d2h_bytes_per_step": int(d2h / Ke),
-                    "steps": Ke, "path": "pinned host ids/dY -> H2D -> emb_forward/backward_exchange -> Y D2H"},
+                    "steps": Ke, "path": "pinned host ids/dY -> H2D (copy stream) -> emb_forward/backward_exchange -> Y D2H (copy stream), pipelined one step"},
             "gpu_launches": int(round(per_step_launch * K)),
             "gpu_launches_per_step": per_step_launch,
             "clocks": clk.summary(),
