@@ -655,6 +655,34 @@ def main():
         e2e_ms = float(tt.item())
     e2e_tok = sum(int((np.asarray(ids_all[(kk + j) % nb][s]) != PAD_ID).sum()) for j in range(Ke) for s in range(world))
     check_err("end-to-end pass")
+
+    # PCIe ceiling of the e2e leg: the same per-step bytes copied with no
+    # compute (H2D on s_h2d, D2H on s_d2h, concurrently), pinned host buffers.
+    hb_in = torch.empty(max(1, h2d // Ke), dtype=torch.uint8).pin_memory()
+    hb_out = torch.empty(max(1, d2h // Ke), dtype=torch.uint8).pin_memory()
+    db_in = torch.empty(hb_in.numel(), dtype=torch.uint8, device=dev)
+    db_out = torch.empty(hb_out.numel(), dtype=torch.uint8, device=dev)
+    Kp = 50
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    s_h2d.wait_event(p0)
+    s_d2h.wait_event(p0)
+    for _ in range(Kp):
+        with torch.cuda.stream(s_h2d):
+            db_in.copy_(hb_in, non_blocking=True)
+        with torch.cuda.stream(s_d2h):
+            hb_out.copy_(db_out, non_blocking=True)
+    stream.wait_stream(s_h2d)
+    stream.wait_stream(s_d2h)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    pcie_ms = p0.elapsed_time(p1) / Kp
+    if world > 1:
+        tt = torch.tensor([pcie_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        pcie_ms = float(tt.item())
+    pcie_roof = (e2e_tok / Ke) / (pcie_ms / 1e3)
     ex.flush()
     err = ex.stats()["err_flags"]
 
@@ -681,7 +709,11 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d / Ke), "d2h_bytes_per_step": int(d2h / Ke),
-                    "steps": Ke, "path": "pinned host ids/dY -> H2D (copy stream) -> emb_forward/backward_exchange -> Y D2H (copy stream), pipelined one step"},
+                    "steps": Ke, "pcie_bound": {"value": pcie_roof, "frac": (e2e_tok / (e2e_ms / 1e3)) / pcie_roof,
+                                                "copy_ms_per_step": pcie_ms,
+                                                "what": "same H2D+D2H bytes per step copied concurrently on the "
+                                                        "two copy streams with no compute"},
+                    "path": "pinned host ids/dY -> H2D (copy stream) -> emb_forward/backward_exchange -> Y D2H (copy stream), pipelined one step"},
             "gpu_launches": int(round(per_step_launch * K)),
             "gpu_launches_per_step": per_step_launch,
             "clocks": clk.summary(),
