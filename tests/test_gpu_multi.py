@@ -28,13 +28,23 @@ def _free_port():
     return p
 
 
+def _launch(n, script, args, timeout):
+    """torchrun on a fresh port; the port probe can race with another process
+    binding it before the rendezvous store does, so EADDRINUSE is retried."""
+    for _ in range(4):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+               os.path.join(ROOT, "tests", script)] + list(args)
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        out = r.stdout + r.stderr
+        if r.returncode == 0 or "EADDRINUSE" not in out:
+            break
+    return r.returncode, out
+
+
 def _run(n, *args, timeout=600):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "dist_worker.py")] + list(args)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0 and out.count("PARITY OK") == n, out[-6000:]
+    rc, out = _launch(n, "dist_worker.py", args, timeout)
+    assert rc == 0 and out.count("PARITY OK") == n, out[-6000:]
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
@@ -83,9 +93,5 @@ def test_dense_queue_multi(n, window):
     window rule (reading R16), mixed fp32 / bf16 blocks."""
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "dense_worker.py"), "--window", str(window)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0 and out.count("DENSE OK") == n, out[-6000:]
+    rc, out = _launch(n, "dense_worker.py", ["--window", str(window)], 300)
+    assert rc == 0 and out.count("DENSE OK") == n, out[-6000:]
