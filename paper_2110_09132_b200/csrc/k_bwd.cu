@@ -479,8 +479,10 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
 #pragma unroll
       for (int j = 0; j < EA; ++j) {
         kk[j] = k0 + j * step;
-        ok[j] = kk[j] < U && (chunk_off[kk[j] + 1] - chunk_off[kk[j]]) == 1;
-        id[j] = ok[j] ? uid[kk[j]] : 0;
+        // uid and chunk_off loads issued together (uid[k] is valid for every k < U)
+        const bool in = kk[j] < U;
+        id[j] = in ? __ldcg(uid + kk[j]) : 0;
+        ok[j] = in && (__ldcg(chunk_off + kk[j] + 1) - __ldcg(chunk_off + kk[j])) == 1;
       }
 #pragma unroll
       for (int j = 0; j < EA; ++j) {
