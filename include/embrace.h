@@ -174,6 +174,31 @@ emb_status emb_get_unique_id(uint8_t* id_out);
 emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8_t* nccl_id,
                           const void* shard_init, emb_stream_t stream);
 
+/* Co-located ranks (DESIGN.md §6 "Co-located mode"): the N contexts of ONE
+ * process share ONE device, so every N > 1 step of the exchange (id push,
+ * peer pull, gradient push, owner merge, scheduled part, flag gates) runs on
+ * a single GPU with the same kernels and the same flag protocol; peers'
+ * regions are plain device pointers instead of CUDA IPC mappings.  For
+ * testing the N > 1 paths without N GPUs; no dense queue (NCCL rejects
+ * duplicate devices).
+ *   emb_sym_base : out, device base of this context's symmetric region
+ *   peer_bases   : host, N device pointers in rank order (emb_sym_base of each
+ *                  rank; own entry NULL or its own base); each must live on
+ *                  cfg->device
+ *   shard_init   : as emb_shard_init; borrowed until `stream` completes
+ * Unlike emb_shard_init this does NOT synchronise: each rank's boot barrier
+ * waits on device for the others, so the caller must issue this for all N
+ * contexts before it synchronises any of their streams, and must drive every
+ * later collective call of all N ranks before synchronising (each context's
+ * work spins, bounded by timeout_ms, on the others' flags).  The N ranks'
+ * streams must run concurrently: with 3 library streams per rank plus the
+ * caller's, set CUDA_DEVICE_MAX_CONNECTIONS >= 4N before CUDA initialises
+ * (streams aliased onto one hardware queue serialise, and a spinning gate
+ * then waits until timeout_ms expires: EMB_ERR_TIMEOUT, never a hang).   */
+emb_status emb_sym_base(emb_ctx* ctx, void** base);
+emb_status emb_shard_init_colocated(emb_ctx* ctx, void* const* peer_bases, const void* shard_init,
+                                    emb_stream_t stream);
+
 /* a1-a4 of SURVEY §8(a): forward exchange of iteration t.
  *   ids : device int32 [n]  this rank's token ids (0 <= id < L)
  *   n   : 0 <= n <= max_tokens
@@ -223,12 +248,16 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
  *   ticket   : out, id for dense_wait
  * Issue rule (identical on every rank, a pure function of the enqueue
  * sequence): after each enqueue, while >= W requests are pending, issue the
- * smallest (priority, seq).  Requires nccl_id at shard init.               */
+ * smallest (priority, seq).  Requires nccl_id at shard init.
+ * Bounded state: completion events are recycled over a ring of 1024 tickets
+ * (EMB_ERR_CAPACITY if the ticket 1024 older is still pending), and the issue
+ * log (EMB_DBG_ISSUE_LOG) keeps the first 65536 issues.                     */
 emb_status dense_allreduce_enqueue(emb_ctx* ctx, void* buf, int64_t count, emb_dtype dtype,
                                    int32_t priority, emb_event_t ready, int64_t* ticket);
 /* Issue every pending request in (priority, seq) order.                      */
 emb_status dense_queue_flush(emb_ctx* ctx);
-/* Make `consumer` wait for the AllReduce of `ticket` (must be issued).       */
+/* Make `consumer` wait for the AllReduce of `ticket` (must be issued, and
+ * fewer than 1024 tickets old: EMB_ERR_STATE otherwise).                     */
 emb_status dense_wait(emb_ctx* ctx, int64_t ticket, emb_stream_t consumer);
 
 /* Make `stream` wait for all outstanding deferred work (scheduled parts) and

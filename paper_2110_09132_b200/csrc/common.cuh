@@ -79,7 +79,6 @@ struct DevCtx {
   int* plan_cnt;          // [2][2]  entries per part
   int* counts;            // [2][N][CNT_W]
   float* scratch;         // [2][N][max_chunks][dw] chunk partials (dw = D sender / d RAW owner)
-  int* slot_ctr;          // [2][N][max_tok]    (unused; reserved)
   float* gcoal;           // [max_tok][D] fp32  sender-coalesced rows of single-chunk uniques (COAL/SPLIT)
   char* stage;            // [2][max_tok][D]    scheduled coalesced rows waiting to be pushed (N > 1)
   float* gc_owner;        // [2][N][max_tok][d] RAW: owner-coalesced rows (fp32)
@@ -247,18 +246,23 @@ __device__ __forceinline__ void wait_all(const DevCtx& c, const uint32_t* flags,
 // Publish value v into slot [c.r] of field `field` (an offset into Flags) of
 // every rank's flags.  Called by ONE thread of the kernel that follows the
 // producer, after griddepcontrol.wait (same stream) or a full graph/event
-// dependency (other stream): the producer grid has COMPLETED, and grid
-// completion includes the end-of-grid system-scope memory flush (the one that
-// makes a finished kernel's stores — local, peer and host-mapped — visible to
-// the host after an event).  Every producer store is therefore performed at
-// system scope before this thread runs, and the flag needs no fence of its
-// own: a relaxed system-scope store suffices.
-// A fence.sys here cost 2-7 us per publish on B200 under concurrent NVLink
-// traffic (kernel trace, profiles/r01_trace_n2.txt).  Stores made by the SAME
-// kernel before a flag (mark) still take fence_acq_rel_sys().
+// dependency (other stream): the producer grid has completed and its stores
+// are visible to this thread.  One fence.acq_rel.sys then orders everything
+// this thread has observed (cumulativity: the producer grid's local and peer
+// stores) before the flag stores at system scope, so a peer that reads the
+// flag with ld.acquire.sys sees the data — the PTX message-passing pattern,
+// without relying on an end-of-grid flush that the memory model does not
+// state.  (Round 1 used relaxed flag stores with no fence: a fence.sc.sys per
+// publish had cost 2-7 us under concurrent NVLink traffic, kernel trace
+// profiles/r01_trace_n2.txt; the build flag EMB_RELAXED_PUBLISH restores that
+// variant for measurement only.)  Stores made by the SAME kernel before a
+// flag (mark) take fence_acq_rel_sys() themselves.
 __device__ __forceinline__ void publish2(const DevCtx& c, size_t off_a, uint32_t va, bool do_a, size_t off_b,
                                          uint32_t vb, bool do_b) {
   if (c.N == 1 || !(do_a || do_b)) return;
+#ifndef EMB_RELAXED_PUBLISH
+  fence_acq_rel_sys();
+#endif
   for (int s = 0; s < c.N; ++s) {
     char* f = reinterpret_cast<char*>(flags_of(c, s));
     if (do_a) st_relaxed_sys(reinterpret_cast<uint32_t*>(f + off_a) + c.r, va);

@@ -88,7 +88,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (cfg->optim == EMB_ADAM) loc += 2 * L * pl->d * 4;
   if (N > 1) loc += 2 * L * N * 8;                               // slotmap
   loc += 2 * L * 4;                                              // nextmark
-  loc += 5 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id slot_ctr | useg chunk_off
+  loc += 3 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id | useg chunk_off
   loc += 2 * N * (size_t)pl->max_chunks * 16 + 2 * N * CNT_W * 4 + 2 * N * (size_t)pl->max_long * 4;
   if (cfg->mode != EMB_BWD_RAW) loc += T * cfg->dim * 4;       // gcoal
   loc += 2 * (size_t)pl->max_chunks * cfg->dim * 4;              // scratch
@@ -109,6 +109,7 @@ struct emb_ctx {
   emb_status poisoned = EMB_OK;
   char* sym = nullptr;
   bool peer_open[EMB_MAX_WORLD] = {};
+  bool colocated = false;  // emb_shard_init_colocated: peers are contexts of this process on this device
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
@@ -123,7 +124,6 @@ struct emb_ctx {
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
-  bool fwd_sort_gated = false;  // the last forward's CTA 0 waited for sort(t) (no GATE_SORTED needed)
   // emb_prefetch: fork point of the next batch's work, recorded before forward(t)
   const int32_t* pf_ids = nullptr;
   int32_t pf_n = -1;
@@ -270,7 +270,6 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.chunk_desc, 2 * N * (size_t)pl.max_chunks * 16);
     if (cfg->mode != EMB_BWD_RAW) ALLOC(c.gcoal, T * cfg->dim * 4);
     ALLOC(c.long_u, 2 * N * (size_t)pl.max_long * 4);
-    ALLOC(c.slot_ctr, 2 * N * T * 4);
     ALLOC(c.counts, 2 * N * CNT_W * 4);
     ALLOC(c.scratch, 2 * (size_t)pl.max_chunks * cfg->dim * 4);
     if (cfg->mode == EMB_BWD_SPLIT && N > 1) ALLOC(c.stage, 2 * T * cfg->dim * pl.esz);
@@ -302,7 +301,8 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least priority
     if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo) != cudaSuccess) goto fail;
     if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
-    if (cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
+    // N == 1 only: at N > 1 every sort runs on aux (co-located ranks keep <= 3 streams each)
+    if (pl.N == 1 && cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, hi) != cudaSuccess) goto fail;
   }
   for (int i = 0; i < 2; ++i) {
     if (cudaEventCreateWithFlags(&ctx->ev_prior[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
@@ -357,6 +357,54 @@ __global__ void boot_kernel(DevCtx c, uint32_t val) {
   for (int s = 0; s < c.N; ++s) wait_flag(c, &flags_of(c, c.r)->boot[s], val, 12 * 16 + s);
 }
 
+// shard copy, zeroed moments and the boot barrier (every rank's shard loaded)
+static emb_status shard_load(emb_ctx* ctx, const void* shard_init, cudaStream_t stream) {
+  const size_t shard_bytes = (size_t)ctx->cfg.vocab * ctx->pl.d * ctx->pl.esz;
+  CKC(ctx, cudaMemcpyAsync(ctx->sym + ctx->pl.lay.shard, shard_init, shard_bytes, cudaMemcpyDeviceToDevice, stream));
+  if (ctx->dc.adam_m) {
+    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_m, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
+    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_v, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
+  }
+  boot_kernel<<<1, 32, 0, stream>>>(ctx->dc, 1u);
+  CKC(ctx, cudaGetLastError());
+  return EMB_OK;
+}
+
+emb_status emb_sym_base(emb_ctx* ctx, void** base) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (!base) return EMB_ERR_INVALID_ARG;
+  *base = ctx->sym;
+  return EMB_OK;
+}
+
+emb_status emb_shard_init_colocated(emb_ctx* ctx, void* const* peer_bases, const void* shard_init,
+                                    emb_stream_t stream_) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  if (ctx->state != ST_CREATED) return EMB_ERR_STATE;
+  if (!shard_init || !peer_bases) return EMB_ERR_INVALID_ARG;
+  CKC(ctx, cudaSetDevice(ctx->cfg.device));
+  for (int s = 0; s < ctx->pl.N; ++s) {
+    if (s == ctx->pl.r) {
+      if (peer_bases[s] != nullptr && peer_bases[s] != ctx->sym) return EMB_ERR_INVALID_ARG;
+      continue;
+    }
+    if (!peer_bases[s]) return EMB_ERR_INVALID_ARG;
+    cudaPointerAttributes a;
+    CKC(ctx, cudaPointerGetAttributes(&a, peer_bases[s]));
+    if (a.type != cudaMemoryTypeDevice || a.device != ctx->cfg.device) return EMB_ERR_INVALID_ARG;
+    ctx->dc.sym[s] = static_cast<char*>(peer_bases[s]);
+  }
+  // no host synchronisation: the boot barrier waits on device for the other
+  // co-located ranks, whose init the caller issues next (embrace.h)
+  st = shard_load(ctx, shard_init, reinterpret_cast<cudaStream_t>(stream_));
+  if (st != EMB_OK) return st;
+  ctx->colocated = true;
+  ctx->state = ST_READY;
+  return EMB_OK;
+}
+
 emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8_t* nccl_id,
                           const void* shard_init, emb_stream_t stream_) {
   emb_status st = ctx_check(ctx);
@@ -374,14 +422,8 @@ emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8
     ctx->dc.sym[s] = static_cast<char*>(p);
     ctx->peer_open[s] = true;
   }
-  const size_t shard_bytes = (size_t)ctx->cfg.vocab * ctx->pl.d * ctx->pl.esz;
-  CKC(ctx, cudaMemcpyAsync(ctx->sym + ctx->pl.lay.shard, shard_init, shard_bytes, cudaMemcpyDeviceToDevice, stream));
-  if (ctx->dc.adam_m) {
-    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_m, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
-    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_v, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
-  }
-  boot_kernel<<<1, 32, 0, stream>>>(ctx->dc, 1u);
-  CKC(ctx, cudaGetLastError());
+  st = shard_load(ctx, shard_init, stream);
+  if (st != EMB_OK) return st;
   CKC(ctx, cudaStreamSynchronize(stream));
   int err = 0;
   CKC(ctx, cudaMemcpy(&err, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
@@ -416,16 +458,13 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   //   already complete (fwd_dd[p]); the forward dedups if so, else it gathers
   //   every token (identical Y).  Waiting would put the aux chain (push, tags,
   //   plan, sort) on the critical path when the sort is the slower side (LM).
-  // (sort_gate = 1 — the forward's CTA 0 waiting for the sort's completion
-  // count at its end instead of a gate kernel — measured: GNMT -0.8 us, LM
-  // +2.9 us at N == 1; a CTA spinning in a wide kernel delays other streams'
-  // launches, see §6 Liveness.  Kept off.)
+  // (The forward's CTA 0 waiting for sort(t) instead of the GATE_SORTED
+  // kernel measured GNMT -0.8 us, LM +2.9 us at N == 1 in round 1: a CTA
+  // spinning in a wide kernel delays other streams' launches, §6 Liveness.)
   const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
-  const int sort_gate = 0;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
-                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, sort_gate, dedup, stream); }));
-  ctx->fwd_sort_gated = sort_gate != 0;
+                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, dedup, stream); }));
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)
@@ -499,8 +538,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // at N == 1 it also checks the prefetch fingerprints.  Enqueued before this
   // backward's aux / side work so that host launch order is also a valid
   // serial order (profilers replay kernels one at a time).
-  if (!ctx->fwd_sort_gated)
-    CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
+  CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
 
   if (N == 1) {
     // N == 1: nothing on the critical path needs the D_next marks (the coalesce
@@ -545,8 +583,11 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // push ids(t+1) -> one gate (publish + wait ids(t+1), and this rank's
     // scheduled push of t-1 past the routing tables) -> D_next tags -> merge
     // plan -> sort(t+1) -> the Alg. 1 tables of t (presentation, last).
-    CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, 0, aux); }));
-    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, 1 | 2 | 4 | 8 | 16, aux));
+    // next_ids == NULL (D_next = ∅): nothing is pushed or published for batch
+    // t+1 here — forward(t+1) pushes, publishes and sorts its own ids — so the
+    // gate only keeps the wait that frees parity p's tags / plan (flag 8)
+    if (next_ids) CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, 0, aux); }));
+    CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, next_ids ? (1 | 2 | 4 | 8 | 16) : (8 | 16), aux));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, 0, aux); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;

@@ -54,14 +54,21 @@ void issue_rule_order(const int32_t* priorities, int32_t n, int32_t window, std:
   rule_flush(pending, issue);
 }
 
+// Completion events live in a ring of RING slots (ticket t -> slot t % RING),
+// recycled as tickets advance, so a long run holds a fixed number of events
+// and bytes; the issue log keeps the first LOG_CAP entries.
+static constexpr int64_t RING = 1024;
+static constexpr size_t LOG_CAP = 1 << 16;
+
 struct DenseQueue {
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   int window = 1;
   int64_t next_seq = 0;
   std::vector<Req> pending;
-  std::vector<cudaEvent_t> done;   // per ticket
-  std::vector<bool> issued;
+  cudaEvent_t done[RING] = {};      // slot of ticket t: t % RING
+  int64_t slot_ticket[RING];        // ticket currently owning the slot (-1: none)
+  bool slot_issued[RING] = {};
   std::vector<int64_t> log;
   emb_status err = EMB_OK;
 };
@@ -78,9 +85,13 @@ DenseQueue* dense_queue_create(const uint8_t* nccl_id, int world, int rank, int 
   }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  if (cudaStreamCreateWithPriority(&q->stream, cudaStreamNonBlocking, hi) != cudaSuccess) {
-    ncclCommDestroy(q->comm);
-    delete q;
+  bool ok = cudaStreamCreateWithPriority(&q->stream, cudaStreamNonBlocking, hi) == cudaSuccess;
+  for (int64_t i = 0; i < RING; ++i) {
+    q->slot_ticket[i] = -1;
+    if (ok) ok = cudaEventCreateWithFlags(&q->done[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+  if (!ok) {
+    dense_queue_destroy(q);
     return nullptr;
   }
   return q;
@@ -94,19 +105,20 @@ static void do_issue(DenseQueue* q, const Req& x) {
     q->err = EMB_ERR_NCCL;
     return;
   }
-  if (cudaEventRecord(q->done[x.seq], q->stream) != cudaSuccess) { q->err = EMB_ERR_CUDA; return; }
-  q->issued[x.seq] = true;
-  q->log.push_back(x.seq);
+  if (cudaEventRecord(q->done[x.seq % RING], q->stream) != cudaSuccess) { q->err = EMB_ERR_CUDA; return; }
+  q->slot_issued[x.seq % RING] = true;
+  if (q->log.size() < LOG_CAP) q->log.push_back(x.seq);
 }
 
 emb_status dense_queue_enqueue(DenseQueue* q, void* buf, int64_t count, emb_dtype dt, int32_t prio,
                                cudaEvent_t ready, int64_t* ticket) {
   if (q->err != EMB_OK) return q->err;
+  const int64_t slot = q->next_seq % RING;
+  // the slot's previous ticket (next_seq - RING) must have been issued
+  if (q->slot_ticket[slot] >= 0 && !q->slot_issued[slot]) return EMB_ERR_CAPACITY;
   Req r{prio, q->next_seq++, buf, count, dt, ready};
-  cudaEvent_t ev;
-  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return q->err = EMB_ERR_CUDA;
-  q->done.push_back(ev);
-  q->issued.push_back(false);
+  q->slot_ticket[slot] = r.seq;
+  q->slot_issued[slot] = false;
   *ticket = r.seq;
   rule_push(q->pending, r, q->window, [&](const Req& x) { do_issue(q, x); });
   return q->err;
@@ -119,9 +131,11 @@ emb_status dense_queue_flush_all(DenseQueue* q) {
 
 emb_status dense_queue_wait(DenseQueue* q, int64_t ticket, cudaStream_t consumer) {
   if (q->err != EMB_OK) return q->err;
-  if (ticket < 0 || ticket >= (int64_t)q->done.size()) return EMB_ERR_INVALID_ARG;
-  if (!q->issued[ticket]) return EMB_ERR_STATE;  // still pending: flush first
-  return cudaStreamWaitEvent(consumer, q->done[ticket], 0) == cudaSuccess ? EMB_OK : EMB_ERR_CUDA;
+  if (ticket < 0 || ticket >= q->next_seq) return EMB_ERR_INVALID_ARG;
+  const int64_t slot = ticket % RING;
+  if (q->slot_ticket[slot] != ticket) return EMB_ERR_STATE;  // expired: RING newer tickets since
+  if (!q->slot_issued[slot]) return EMB_ERR_STATE;          // still pending: flush first
+  return cudaStreamWaitEvent(consumer, q->done[slot], 0) == cudaSuccess ? EMB_OK : EMB_ERR_CUDA;
 }
 
 emb_status dense_queue_wait_all(DenseQueue* q, cudaStream_t consumer) {
@@ -140,7 +154,8 @@ void dense_queue_issue_log(DenseQueue* q, std::vector<int64_t>* log) { *log = q-
 void dense_queue_destroy(DenseQueue* q) {
   if (!q) return;
   if (q->stream) cudaStreamSynchronize(q->stream);
-  for (cudaEvent_t e : q->done) cudaEventDestroy(e);
+  for (cudaEvent_t e : q->done)
+    if (e) cudaEventDestroy(e);
   if (q->comm) ncclCommDestroy(q->comm);
   if (q->stream) cudaStreamDestroy(q->stream);
   delete q;

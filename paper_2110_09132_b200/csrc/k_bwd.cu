@@ -11,15 +11,16 @@
 // B200 design.  Rows are addressed by the sender's
 // unique index i (ascending unique ids from the sort); the prior / scheduled
 // class of a row is the D_next mark of its id.
-//   coal     sender-side segmented reduce of dY in fp32, one warp per chunk of
-//            <= C rows (2 in flight), ascending positions; chunks of multi-
-//            chunk (Zipf-head) uniques leave fp32 partials that the CTA which
-//            completes the unique combines in a fixed order (deterministic, no
-//            float atomics).  Coalesced rows are parked in shared memory and
-//            emitted by the whole CTA:
+//   coal_reduce  sender-side segmented reduce of dY in fp32, one warp per
+//            reduce chunk of <= C rows of one unique, ascending positions; a
+//            single-chunk unique's sum goes to gcoal, a multi-chunk (Zipf-head)
+//            unique's chunk sums to scratch (no float atomics).
+//   coal_apply   Zipf-head partials combined per (unique, column slice) in a
+//            fixed order (deterministic); then per coalesced row and 16-byte
+//            chunk:
 //              N == 1  optimizer step applied in place (one source = the
 //                      merged gradient: no exchange, no merge kernel);
-//              N > 1   rounded to the wire dtype and stored straight into each
+//              N > 1   rounded to the wire dtype and stored straight into the
 //                      owner's receive row i over NVLink (prior rows), or into
 //                      the local stage (scheduled rows) — COALESCE +
 //                      INDEX_SELECT + AlltoAll in one pass.
@@ -175,97 +176,6 @@ __device__ __forceinline__ void opt_math(const DevCtx& c, float alpha, const flo
     mm[i] = mm[i] + om_b1 * (gs - mm[i]);
     vv[i] = vv[i] + om_b2 * (gs * gs - vv[i]);
     w[i] = w[i] - alpha * mm[i] * rcp_approx(sqrt_approx(vv[i]) + c.eps);
-  }
-}
-
-// CTA-cooperative emission of coalesced rows parked in shared memory: row j
-// (D floats at rows + j*D) is unique index ks[j] (skipped if < 0) of this
-// rank's source, id us[j], class pr[j] (1 = prior / single part).
-//   N == 1: the coalesced row IS the merged gradient of its id (one source):
-//           the optimizer step is applied here.  The row is first rounded to
-//           the wire dtype — the same rounding point as N > 1 (reading R11).
-//   N > 1:  round to the wire dtype and store the column slices into the
-//           owners' receive row i (prior rows, NVLink) or the stage (scheduled).
-// Every thread handles EU (row, 16-byte chunk) items, state loads first.
-#ifndef EMB_EU
-#define EMB_EU 8
-#endif
-template <int DT>
-__device__ __forceinline__ void emit_rows(const DevCtx& c, int p, const float* rows, const int* ks, const int* us,
-                                          const int* pr, int nrows, float alpha) {
-  constexpr int EPV = Vec<DT>::EPV;
-  constexpr int EU = EMB_EU / EPV;  // items in flight: 2 fp32 / 1 bf16
-  const int total = nrows * c.cpr;
-  const size_t slice_bytes = (size_t)c.d * c.esz, row_bytes = (size_t)c.D * c.esz;
-  const bool adam = (c.optim == ADAM);
-  for (int b0 = threadIdx.x; b0 < total; b0 += blockDim.x * EU) {
-    int ii[EU], cc[EU];
-    bool ok[EU];
-#pragma unroll
-    for (int j = 0; j < EU; ++j) {
-      const int it = b0 + j * blockDim.x;
-      ii[j] = it / c.cpr;
-      cc[j] = it - ii[j] * c.cpr;
-      ok[j] = it < total && ks[ii[j]] >= 0;
-    }
-    if (c.N == 1) {
-      uint4 wr[EU];
-      float mm[EU][EPV], vv[EU][EPV];
-#pragma unroll
-      for (int j = 0; j < EU; ++j) {
-        if (!ok[j]) continue;
-        const size_t u = (size_t)us[ii[j]];
-        wr[j] = ld16(shard_of(c, c.r) + u * slice_bytes + (size_t)cc[j] * 16);
-        if (adam) {
-#pragma unroll
-          for (int x = 0; x < EPV; x += 4) {
-            const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + cc[j] * EPV + x);
-            const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + cc[j] * EPV + x);
-            mm[j][x] = m4.x; mm[j][x + 1] = m4.y; mm[j][x + 2] = m4.z; mm[j][x + 3] = m4.w;
-            vv[j][x] = v4.x; vv[j][x + 1] = v4.y; vv[j][x + 2] = v4.z; vv[j][x + 3] = v4.w;
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < EU; ++j) {
-        if (!ok[j]) continue;
-        const size_t u = (size_t)us[ii[j]];
-        float g[EPV], w[EPV];
-        const float* src = rows + (size_t)ii[j] * c.D + cc[j] * EPV;
-#pragma unroll
-        for (int x = 0; x < EPV; ++x) g[x] = src[x];
-        Vec<DT>::unpack(Vec<DT>::pack(g), g);  // wire rounding point
-        Vec<DT>::unpack(wr[j], w);
-        opt_math<EPV>(c, alpha, g, w, mm[j], vv[j]);
-        st16(shard_of(c, c.r) + u * slice_bytes + (size_t)cc[j] * 16, Vec<DT>::pack(w));
-        if (adam) {
-#pragma unroll
-          for (int x = 0; x < EPV; x += 4) {
-            *reinterpret_cast<float4*>(c.adam_m + u * c.d + cc[j] * EPV + x) =
-                make_float4(mm[j][x], mm[j][x + 1], mm[j][x + 2], mm[j][x + 3]);
-            *reinterpret_cast<float4*>(c.adam_v + u * c.d + cc[j] * EPV + x) =
-                make_float4(vv[j][x], vv[j][x + 1], vv[j][x + 2], vv[j][x + 3]);
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < EU; ++j) {
-        if (!ok[j]) continue;
-        const int k = ks[ii[j]], c16 = cc[j];
-        float g[EPV];
-        const float* src = rows + (size_t)ii[j] * c.D + c16 * EPV;
-#pragma unroll
-        for (int x = 0; x < EPV; ++x) g[x] = src[x];
-        const uint4 val = Vec<DT>::pack(g);
-        if (pr[ii[j]]) {
-          const int s = c16 / c.cps, cs = c16 - s * c.cps;
-          st16(recv_of(c, s, p, c.r) + (size_t)k * slice_bytes + (size_t)cs * 16, val);
-        } else {
-          st16(c.stage + ((size_t)p * c.max_tok + k) * row_bytes + (size_t)c16 * 16, val);
-        }
-      }
-    }
   }
 }
 

@@ -29,7 +29,7 @@ static constexpr int FWD_ROWS = EMB_FWD_ROWS;  // rows in flight per warp
 template <int V>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* __restrict__ ids, int n,
                                                           char* __restrict__ out, int p, int prefetched,
-                                                          int sort_gate, int dedup) {
+                                                          int dedup) {
   EMB_TR_ENTRY();
   pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
@@ -63,13 +63,10 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     if (tid == 0 && *ntok_of(c, c.r, p, c.r) != n) atomicOr(c.err, ERR_STATE);
   }
   // N == 1 and prefetched: the sort of this batch read next_ids directly (no
-  // copy to order against): the ids are fingerprinted after the gather (off
-  // the gather's critical path); the gate before the coalesce compares
-#ifndef EMB_FWD_FP_LATE
-#define EMB_FWD_FP_LATE 0  // measured (N = 1): late LM 20.68 -> 20.62 us, BERT 44.04 -> 44.33 us; kept off
-#endif
-  const bool fingerprint = prefetched && c.N == 1;
-  if (!EMB_FWD_FP_LATE && fingerprint) {
+  // copy to order against): the ids are fingerprinted here; the gate before
+  // the coalesce compares (k_gate.cu GATE_SORTED).  (Fingerprinting after the
+  // gather measured mixed in round 1 — LM -0.06 us, BERT +0.3 us — not kept.)
+  if (prefetched && c.N == 1) {
     unsigned h = 0;
     for (int j = tid; j < n; j += nth) h += prefetch_hash(__ldg(ids + j), j);
 #pragma unroll
@@ -175,28 +172,12 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
       }
     }
   }
-  if (EMB_FWD_FP_LATE && fingerprint) {
-    unsigned h = 0;
-    for (int j = tid; j < n; j += nth) h += prefetch_hash(__ldg(ids + j), j);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-    if ((threadIdx.x & 31) == 0 && h) atomicAdd(&c.fp[p * 4 + 0], h);
-    if (tid == 0) atomicAdd(&c.fp[p * 4 + 1], (unsigned)n);
-  }
-  if (sort_gate && blockIdx.x == 0 && threadIdx.x == 0) {
-    // the coalesce that follows needs sort(t) (aux stream, launched one
-    // iteration ahead): CTA 0 waits for it here instead of a gate kernel
-    // between the two (one kernel boundary less on the main stream), then
-    // lets the side stream start this iteration's backward work
-    wait_local(c, c.sort_count + p, (t + 1) / 2, 9 * 16 + 1);  // one sort of parity p per iteration
-    st_release_gpu(c.seq + SEQ_BWD, t);
-  }
   EMB_TR_END(0, t);
   pdl_trigger();
 }
 
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, int sort_gate, int dedup, cudaStream_t s) {
+                       int prefetched, int dedup, cudaStream_t s) {
   const int warps = (n + FWD_ROWS - 1) / FWD_ROWS;
   int grid = (warps + FWD_THREADS / 32 - 1) / (FWD_THREADS / 32);
   if (grid < 1) grid = 1;
@@ -204,10 +185,10 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   const int V = (c.cpr + 31) / 32;
   char* o = static_cast<char*>(out);
   const dim3 g(grid), b(FWD_THREADS);
-  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
-  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
-  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
-  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched, sort_gate, dedup);
+  if (V <= 1) return launch_pdl(fwd_kernel<1>, g, b, 0, s, c, ids, n, o, p, prefetched, dedup);
+  if (V <= 2) return launch_pdl(fwd_kernel<2>, g, b, 0, s, c, ids, n, o, p, prefetched, dedup);
+  if (V <= 4) return launch_pdl(fwd_kernel<4>, g, b, 0, s, c, ids, n, o, p, prefetched, dedup);
+  if (V <= 8) return launch_pdl(fwd_kernel<8>, g, b, 0, s, c, ids, n, o, p, prefetched, dedup);
   return cudaErrorInvalidValue;
 }
 

@@ -80,7 +80,10 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
       if (j < n_next) dst[j] = v[q];
     }
   }
-  if (k == 0 && threadIdx.x == 0) {
+  // next_ids == NULL (N == 1 only: the side stream's iteration counter above
+  // still advances): no copy and no count — forward(t+1) writes its own count
+  // on the main stream, which a late store of 0 here would overwrite
+  if (next_ids != nullptr && k == 0 && threadIdx.x == 0) {
     *ntok_of(c, s, p ^ 1, c.r) = n_next;
     atomicAdd(&c.stats[2 * c.N + s], (unsigned long long)n_next * 4ull);
   }

@@ -83,7 +83,7 @@ cudaError_t launch_gate(const DevCtx& c, int p, int kind, int flag_arg, cudaStre
 // a1-a4: forward (publish prior_done/def_done of earlier iterations, alpha_t,
 // id push or prefetch check, wait for every owner, pull-gather)
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
-                       int prefetched, int sort_gate, int dedup, cudaStream_t s);
+                       int prefetched, int dedup, cudaStream_t s);
 // a6: per-source sort by (dropped, id, position), unique ids, reduce chunks,
 // owner routing (slotmap) — auxiliary stream, one iteration ahead
 cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, int from_bwd, bool key64,

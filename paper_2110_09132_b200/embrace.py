@@ -31,7 +31,7 @@ MODES = {"raw": EMB_BWD_RAW, "coal": EMB_BWD_COAL, "split": EMB_BWD_SPLIT}
 
 EXPORTED = [
     "emb_status_str", "emb_workspace_bytes", "emb_create", "emb_ipc_handle", "emb_get_unique_id",
-    "emb_shard_init", "emb_forward_exchange", "emb_prefetch", "emb_backward_exchange", "dense_allreduce_enqueue",
+    "emb_shard_init", "emb_sym_base", "emb_shard_init_colocated", "emb_forward_exchange", "emb_prefetch", "emb_backward_exchange", "dense_allreduce_enqueue",
     "dense_queue_flush", "dense_wait", "emb_flush", "emb_join", "emb_profile", "emb_profile_read",
     "emb_get_stats", "emb_debug_copy", "emb_state_ptr", "emb_queue_issue_order", "emb_shard_destroy",
 ]
@@ -87,6 +87,8 @@ def lib():
             "emb_ipc_handle": [vp, u8p],
             "emb_get_unique_id": [u8p],
             "emb_shard_init": [vp, u8p, u8p, vp, vp],
+            "emb_sym_base": [vp, ctypes.POINTER(vp)],
+            "emb_shard_init_colocated": [vp, ctypes.POINTER(vp), vp, vp],
             "emb_forward_exchange": [vp, vp, i32, vp, vp],
             "emb_backward_exchange": [vp, vp, vp, i32, vp],
             "emb_prefetch": [vp, vp, i32, vp],
@@ -174,6 +176,17 @@ def emb_get_unique_id():
 def emb_shard_init(ctx, peer_handles, nccl_id, shard_init, stream=None):
     _ck(lib().emb_shard_init(ctx, _bytes_arg(peer_handles), _bytes_arg(nccl_id), _ptr(shard_init),
                              _stream(stream)), "emb_shard_init")
+
+
+def emb_sym_base(ctx):
+    p = ctypes.c_void_p()
+    _ck(lib().emb_sym_base(ctx, ctypes.byref(p)), "emb_sym_base")
+    return p.value
+
+
+def emb_shard_init_colocated(ctx, peer_bases, shard_init, stream=None):
+    arr = (ctypes.c_void_p * len(peer_bases))(*[b or None for b in peer_bases])
+    _ck(lib().emb_shard_init_colocated(ctx, arr, _ptr(shard_init), _stream(stream)), "emb_shard_init_colocated")
 
 
 def emb_forward_exchange(ctx, ids, out, stream=None):

@@ -47,12 +47,17 @@ class EmbraceExchange:
         self.d = dim // world
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.ctx = E.emb_create(self.cfg)
+        self._closed = False
+        # borrowed device buffers (embrace.h): next_ids / the prefetch argument
+        # may be read by the library's streams until the next backward call
+        self._borrowed = []
+        if shard_init is None:          # co-located ranks: make_colocated() initialises
+            return
         handles = exchange_bytes(E.emb_ipc_handle(self.ctx), world, group)
         nccl_id = None
         if dense_queue:
             nccl_id = broadcast_bytes(E.emb_get_unique_id() if rank == 0 else None, world, 0, group)
         E.emb_shard_init(self.ctx, b"".join(handles), nccl_id, shard_init.contiguous())
-        self._closed = False
 
     # -------------------------------------------------------------- exchange
     def forward(self, ids, out=None, stream=None):
@@ -63,9 +68,13 @@ class EmbraceExchange:
 
     def prefetch(self, next_ids, stream=None):
         E.emb_prefetch(self.ctx, next_ids, stream)
+        self._borrowed.append(next_ids)
 
     def backward(self, grad_out, next_ids=None, stream=None):
         E.emb_backward_exchange(self.ctx, grad_out, next_ids, stream)
+        # what the previous backward borrowed is released by this call; keep
+        # this call's next_ids (and grad_out, read in stream order) alive
+        self._borrowed = [next_ids, grad_out]
 
     def flush(self, stream=None):
         E.emb_flush(self.ctx, stream)
@@ -96,7 +105,29 @@ class EmbraceExchange:
     def dense_wait(self, ticket, stream=None):
         E.dense_wait(self.ctx, ticket, stream)
 
+    def sym_base(self):
+        return E.emb_sym_base(self.ctx)
+
     def close(self):
         if not self._closed:
             E.emb_shard_destroy(self.ctx)
             self._closed = True
+
+
+def make_colocated(vocab, dim, shards, streams, *, device=None, **kw):
+    """N ranks of the exchange in ONE process on ONE device (co-located mode,
+    embrace.h emb_shard_init_colocated): rank r holds shards[r] ([L, D/N]) and
+    runs on streams[r].  Every N > 1 code path (peer pull, gradient push, owner
+    merge, scheduled part, flag gates) runs with the same kernels as across
+    GPUs.  The caller must drive all N ranks' calls before synchronising any
+    stream, and needs CUDA_DEVICE_MAX_CONNECTIONS >= 4N set before CUDA
+    initialises.  Returns the N EmbraceExchange objects (rank order)."""
+    N = len(shards)
+    device = torch.cuda.current_device() if device is None else device
+    exs = [EmbraceExchange(vocab, dim, None, world=N, rank=r, device=device, **kw) for r in range(N)]
+    bases = [x.sym_base() for x in exs]
+    for r, x in enumerate(exs):
+        sh = shards[r].contiguous()
+        E.emb_shard_init_colocated(x.ctx, bases, sh, streams[r])
+        x._borrowed = [sh]              # read by the stream-ordered copy
+    return exs

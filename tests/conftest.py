@@ -1,7 +1,12 @@
 import os
 import sys
 
-import pytest
+# Co-located multi-rank tests (tests/test_gpu_colocated.py) run N ranks'
+# streams concurrently on one GPU: every stream needs its own hardware queue
+# (embrace.h emb_shard_init_colocated).  Must be set before CUDA initialises.
+os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

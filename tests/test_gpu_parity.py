@@ -10,7 +10,7 @@ import pytest
 from synthetic import get_config
 from synthetic.workloads import Config
 
-from _harness import parity_run
+from _harness import graph_parity, parity_run
 
 pytestmark = pytest.mark.gpu
 
@@ -158,3 +158,44 @@ def test_prefetch_split_adam():
     parity_run(cfg, N=1, mode="split", iters=4, optim="adam", lr=1e-3, prefetch=True)
     parity_run(dataclasses.replace(get_config("lstm_lm"), batch=16), N=1, mode="split", iters=3,
                rows_sample=512, prefetch=True)
+
+
+# ---------------------------------------------------------------- round 2: free-running, pipelined, graph
+
+def test_free_running_50_iterations_fp32_adam():
+    """50 iterations with no resync: the oracle runs free, the tolerance is the
+    sigma accumulated over the iterations that touched a row (tests/_metric.py),
+    so the Adam step counter to t = 50 and every row's history are checked."""
+    cfg = Config("free", 2000, 64, "fp32", 8, 24, 6, optim="adam", lr=1e-3, zipf_s=1.1)
+    parity_run(cfg, N=1, mode="split", iters=50, free=True)
+
+
+def test_free_running_bf16_adam():
+    parity_run(_small("bert_large", batch=2), N=1, mode="split", iters=12, free=True)
+
+
+@pytest.mark.parametrize("prefetch", [False, True])
+def test_pipelined_n1_lm(prefetch):
+    """LM-shaped, 6 iterations back to back without flush, NULL next_ids mid-run."""
+    parity_run(_small("lstm_lm", batch=16), N=1, mode="split", iters=6, prefetch=prefetch, pipelined=True,
+               null_at=(2,), rows_sample=1024)
+
+
+@pytest.mark.parametrize("name", ["tiny", "gnmt"])
+def test_graph_replay_n1(name):
+    """The bench's timed path (CUDA graph of a cycle of steps, replayed) against the oracle."""
+    cfg = get_config(name) if name == "tiny" else _small(name, batch=8)
+    errs, iters = graph_parity(cfg, N=1)
+    assert iters == 3 + 2 * 4 + 1
+
+
+@pytest.mark.slow
+def test_graph_replay_lm_full_size():
+    """BASELINE configs[1] at full size through the graph path bench.py times."""
+    graph_parity(get_config("lstm_lm"), N=1, warm=3, nb=4, replays=2)
+
+
+def test_backward_null_then_forward_no_flush():
+    """backward(next_ids = NULL) followed by forward without a
+    flush in between must not lose the next batch's gradient."""
+    parity_run(get_config("tiny"), N=1, mode="split", iters=5, null_at=(0, 1, 2), pipelined=True)
