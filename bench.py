@@ -24,7 +24,14 @@ import sys
 import threading
 import time
 
-import numpy as np
+# The CPU baseline (the oracle) is single-threaded by construction: the thread
+# pools of every BLAS NumPy may link are pinned to one thread BEFORE NumPy is
+# imported (setting them later has no effect), and cpu_baseline() pins the
+# process to one core while it runs.
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "NUMEXPR_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -236,40 +243,73 @@ def oracle_step_fn(cfg, N, mode, budget_s):
     return (lambda k: run(k, frac)), desc
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class pinned_core:
+    """Pin this process to one core (the lowest it may run on) for the block."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
+def host_info(pin):
+    return {"cores": 1, "pinned_core": pin.core, "host_cpu_count": os.cpu_count(), "cpu_model": cpu_model(),
+            "threads_env": {v: os.environ.get(v) for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                                              "MKL_NUM_THREADS")}}
+
+
 def cpu_baseline(cfg, N, mode, seconds=12.0):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    step, desc = oracle_step_fn(cfg, N, mode, budget_s=seconds / 3)
-    toks, k = 0, 1
-    t0 = time.perf_counter()
-    while True:
-        toks += step(k)
-        k += 1
-        el = time.perf_counter() - t0
-        if el > seconds or k > 200:
-            break
-    return {"value": toks / el, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{desc}; {k - 1} timed steps in {el:.1f} s (single-threaded NumPy)"}
+    with pinned_core() as pin:
+        step, desc = oracle_step_fn(cfg, N, mode, budget_s=seconds / 3)
+        toks, k = 0, 1
+        t0 = time.perf_counter()
+        while True:
+            toks += step(k)
+            k += 1
+            el = time.perf_counter() - t0
+            if el > seconds or k > 200:
+                break
+    out = {"value": toks / el, "unit": "tokens/s", "kind": "oracle",
+           "sample": f"{desc}; {k - 1} timed steps in {el:.1f} s (single-threaded NumPy, pinned to one core)"}
+    out.update(host_info(pin))
+    return out
 
 
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    step, desc = oracle_step_fn(cfg, world, args.mode, budget_s=1.0)
-    for k in range(args.warmup):
-        step(k)
-    toks = 0
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        toks += step(args.warmup + k)
-    el = time.perf_counter() - t0
+    with pinned_core() as pin:
+        step, desc = oracle_step_fn(cfg, world, args.mode, budget_s=1.0)
+        for k in range(args.warmup):
+            step(k)
+        toks = 0
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            toks += step(args.warmup + k)
+        el = time.perf_counter() - t0
     val = toks / el
+    cpu = {"value": val, "unit": "tokens/s", "kind": "oracle", "sample": desc}
+    cpu.update(host_info(pin))
     line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name} (oracle on host cores)", "mode": args.mode, "ranks": world},
             "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "cpu_baseline": cpu,
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -521,6 +561,53 @@ def main():
                  for j in range(K) for s in range(world))   # cycles are whole, so batch order is irrelevant
     value = nonpad / (t_max / 1e3)
 
+    # ---------------- step-time distribution, with and without the CUDA graph:
+    # per-replay events (one cycle of nb steps each) and per-step events of an eager pass; every
+    # step's batch index stays in sequence (replays are whole cycles, eager steps continue from kk)
+    def _max_over_ranks(xs):
+        if world == 1:
+            return xs
+        tt = torch.tensor(xs, device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return tt.tolist()
+
+    dist_t = {}
+    R = max(4, min(64, K // max(nb, 1)))
+    if graph is not None:
+        # realign the batch sequence with the captured cycle (the graph's first
+        # forward expects the ids promised by the step before it)
+        for j in range((k0 - kk) % nb):
+            step(kk + j)
+        kk += (k0 - kk) % nb
+        barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
+        evs[0].record(stream)
+        for i in range(R):
+            graph.replay()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        per = _max_over_ranks([evs[i].elapsed_time(evs[i + 1]) * 1e3 / nb for i in range(R)])
+        dist_t["graph"] = {"mean_us": round(statistics.mean(per), 3), "median_us": round(statistics.median(per), 3),
+                           "samples": R, "unit": "us per step (per-replay events / steps per replay)"}
+    Ee = min(K, 400)
+    barrier()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(Ee + 1)]
+    evs[0].record(stream)
+    for j in range(Ee):
+        step(kk + j)
+        evs[j + 1].record(stream)
+    E.emb_join(ex.ctx, stream)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    per = _max_over_ranks([evs[j].elapsed_time(evs[j + 1]) * 1e3 for j in range(Ee)])
+    tot = _max_over_ranks([evs[0].elapsed_time(e_end) * 1e3 / Ee])[0]
+    dist_t["eager"] = {"mean_us": round(tot, 3), "median_us": round(statistics.median(per), 3), "samples": Ee,
+                       "unit": "us per step (mean = whole pass incl. deferred tail / steps; median of per-step "
+                               "events on the caller's stream)"}
+    kk += Ee
+    check_err("step-time distribution")
+
     # ---------------- per-kernel CUDA-event profile (separate, eager, not part of `value`)
     E.emb_profile(ex.ctx, True)
     P = args.profile_steps
@@ -572,6 +659,14 @@ def main():
     step_hbm = sum(v[0] for v in alg.values())
     step_nvl = sum(v[1] for v in alg.values())
     t_roof_us = max(step_hbm / (hbm_peak * 1e9), step_nvl / (nvl_peak * 1e9) if world > 1 else 0) * 1e6
+    # forward NVLink bytes, two conventions: the volume a deduplicating pull must
+    # move ((N-1) * distinct rows * d * e, counted above) and SURVEY §8(d)'s plain
+    # AlltoAll ((N-1) * T_r * d * e, the paper's forward, reading R10)
+    esz_ = 2 if cfg.dtype == "bf16" else 4
+    fwd_plain = sum((world - 1) * len(ids_all[(k_prof + j) % nb][rank]) * (cfg.D // world) * esz_
+                    for j in range(P)) / P
+    step_nvl_plain = step_nvl - alg.get("fwd_pull_gather", (0, 0))[1] + fwd_plain
+    t_roof_plain_us = max(step_hbm / (hbm_peak * 1e9), step_nvl_plain / (nvl_peak * 1e9) if world > 1 else 0) * 1e6
     ms_per_step = t_max / K
 
     # ---------------- end to end through the C ABI with host buffers (pinned)
@@ -693,7 +788,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "bf16"}[cfg.dtype], "data": "synthetic",
             "config": {"workload": f"{cfg.name}: L={cfg.L} D={cfg.D} {cfg.dtype} table, "
                                    + (f"packed <= {cfg.seq_len} tokens" if cfg.packed else
                                       f"{cfg.batch}x{cfg.seq_len} Zipf({cfg.zipf_s}) ids") + " per rank",
@@ -704,7 +799,13 @@ def main():
             "roofline": roof,
             "step_roofline": {"t_roof_us": round(t_roof_us, 3), "t_step_us": round(ms_per_step * 1e3, 3),
                               "frac": round(t_roof_us / (ms_per_step * 1e3), 4),
-                              "hbm_bytes": int(step_hbm), "nvlink_bytes": int(step_nvl)},
+                              "hbm_bytes": int(step_hbm), "nvlink_bytes": int(step_nvl),
+                              "fwd_nvlink_convention": "distinct rows: (N-1) u_r d e",
+                              "plain_alltoall": {"nvlink_bytes": int(step_nvl_plain),
+                                                 "t_roof_us": round(t_roof_plain_us, 3),
+                                                 "frac": round(t_roof_plain_us / (ms_per_step * 1e3), 4),
+                                                 "fwd_nvlink_convention": "SURVEY §8(d): (N-1) T_r d e"}},
+            "step_time": dist_t,
             "kernels": kern,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",

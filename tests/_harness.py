@@ -398,7 +398,8 @@ def graph_parity(cfg, N=1, mode="split", warm=3, nb=4, replays=2, device=0, colo
         torch.cuda.synchronize()
         for _ in range(replays):
             for g, s in graphs:
-                g.replay()
+                with torch.cuda.stream(s):      # replay() launches on the CURRENT stream
+                    g.replay()
             seq.extend((warm + j) % nb for j in range(nb))
         b = (warm + replays * nb) % nb
         for r, ex, s in rk.items():
