@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--graph-no-prefetch", action="store_true",
+                    help="capture the graph without emb_prefetch (round-1 timed path)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=64)
     ap.add_argument("--dense-queue", type=int, default=0, metavar="W",
@@ -519,6 +521,8 @@ def main():
             with torch.cuda.graph(g, stream=cap_stream):
                 for j in range(nb):
                     b = (k0 + j) % nb
+                    if not args.graph_no_prefetch:   # the paper's prefetch, as in step()
+                        E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], cap_stream)
                     E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], cap_stream)
                     E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], cap_stream)
                 E.emb_join(ex.ctx, cap_stream)

@@ -110,6 +110,8 @@ struct emb_ctx {
   char* sym = nullptr;
   bool peer_open[EMB_MAX_WORLD] = {};
   bool colocated = false;  // emb_shard_init_colocated: peers are contexts of this process on this device
+  bool sort_join = true;    // N == 1, prefetched: the forward waits for its sort's event (no GATE_SORTED kernel)
+  bool fwd_joined = false;  // the last forward did
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
@@ -173,6 +175,13 @@ static cudaError_t gate(emb_ctx* ctx, int p, int kind, int flag_arg, cudaStream_
     }                                                                                   \
   } while (0)
 
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  const int x = atoi(v);
+  return x < lo ? lo : (x > hi ? hi : x);
+}
+
 static emb_status ctx_check(emb_ctx* ctx) {
   if (!ctx) return EMB_ERR_INVALID_ARG;
   if (ctx->poisoned != EMB_OK) return ctx->poisoned;
@@ -231,6 +240,10 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   ctx->lc.nsm = nsm > 0 ? nsm : 148;
+  // tuning knobs (measured defaults): forward grid cap per SM,
+  // and how a prefetched N == 1 forward orders itself after its sort
+  ctx->lc.fwd_per_sm = env_int("EMB_FWD_GRID_PER_SM", 4, 1, 32);
+  ctx->sort_join = env_int("EMB_SORT_JOIN", 1, 0, 1) != 0;
 
   DevCtx& c = ctx->dc;
   memset(&c, 0, sizeof(c));
@@ -462,6 +475,16 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // kernel measured GNMT -0.8 us, LM +2.9 us at N == 1 in round 1: a CTA
   // spinning in a wide kernel delays other streams' launches, §6 Liveness.)
   const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
+  // N == 1, prefetched: sort(t) was launched by backward(t-1) one step ago.
+  // The forward takes a real stream dependency on it (an event join: a graph
+  // edge when captured) instead of a GATE_SORTED spin kernel before the
+  // coalesce — the coalesce is ordered after it through the forward.  A spin
+  // in the forward's last CTA instead was measured to deadlock under CUDA
+  // graphs (the graph may serialise the sort behind the spinning forward;
+  // profiles/r02_tune), so no spin crosses a stream here.
+  const bool join = pre && ctx->pl.N == 1 && ctx->sort_join && ctx->sort_pending[p];
+  if (join) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
+  ctx->fwd_joined = join;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
                  [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, dedup, stream); }));
@@ -538,7 +561,10 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // at N == 1 it also checks the prefetch fingerprints.  Enqueued before this
   // backward's aux / side work so that host launch order is also a valid
   // serial order (profilers replay kernels one at a time).
-  CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
+  // (N == 1 prefetched: the forward already joined the sort's event — the
+  // coalesce checks the prefetch fingerprints in its CTA 0.)
+  if (!ctx->fwd_joined)
+    CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
 
   if (N == 1) {
     // N == 1: nothing on the critical path needs the D_next marks (the coalesce

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
   const uint32_t t = c.t_rec[p];
   (void)t;
   EMB_TR_BEGIN(3, t);
+  EMB_TR_WAITED(3, t);
   const int NCH = counts_of(c, p, r)[CNT_NCH];
   const int4* desc = c.chunk_desc + pn(c, p, r) * (size_t)c.max_chunks;
   const int* perm = c.perm + pn(c, p, r) * (size_t)c.max_tok;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
     // bit 1, SPLIT N > 1: the D_next tags of t+1 (marktag, aux) are complete
     if (gate_flags & 1) {
       unsigned* f = c.fp + p * 4;
-      if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
+      if (__ldcg(f) != __ldcg(f + 2) || __ldcg(f + 1) != __ldcg(f + 3)) atomicOr(c.err, ERR_STATE);
       f[0] = f[1] = f[2] = f[3] = 0;
     }
     if (gate_flags & 2) wait_local(c, c.marked + p, t, 8 * 16 + 1);
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
   EMB_TR_BEGIN(16, t);
+  EMB_TR_WAITED(16, t);
   const int* cnt = counts_of(c, p, r);
   const int U = cnt[CNT_U], NLONG = cnt[CNT_NLONG];
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -421,6 +423,7 @@ __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
   EMB_TR_BEGIN(5, t);
+  EMB_TR_WAITED(5, t);
   const int U = counts_of(c, p, r)[CNT_U];
   const int* uid = c.uid + pn(c, p, r) * (size_t)c.max_tok;
   const size_t row_bytes = (size_t)c.D * c.esz, slice_bytes = (size_t)c.d * c.esz;
@@ -548,6 +551,7 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
   const uint32_t t = c.t_rec[p];
   (void)t;
   EMB_TR_BEGIN(part ? 6 : 4, t);
+  EMB_TR_WAITED(part ? 6 : 4, t);
   // N > 1: every sender's pass of this part completed (the gate before this
   // kernel waited for their pub flags).  Items: this part's plan entries (one
   // per distinct id: the id and its unique index at every source, plan_kernel).

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
   pdl_wait();
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
   EMB_TR_BEGIN(0, t);
+  EMB_TR_WAITED(0, t);
   EMB_TR_AT(0, t, 4);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nth = gridDim.x * blockDim.x;
@@ -181,7 +182,7 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
   const int warps = (n + FWD_ROWS - 1) / FWD_ROWS;
   int grid = (warps + FWD_THREADS / 32 - 1) / (FWD_THREADS / 32);
   if (grid < 1) grid = 1;
-  if (grid > L.nsm * 4) grid = L.nsm * 4;  // waits inside: bounded, leaves room for other streams
+  if (grid > L.nsm * L.fwd_per_sm) grid = L.nsm * L.fwd_per_sm;  // leaves room for other streams
   const int V = (c.cpr + 31) / 32;
   char* o = static_cast<char*>(out);
   const dim3 g(grid), b(FWD_THREADS);

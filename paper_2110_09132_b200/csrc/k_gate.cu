@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // owner (this rank included) must have applied both parts.
         const uint32_t t = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, t);
+        EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
         publish2(c, EMB_FLAG_OFF(prior_done), t - 1, t >= 2, EMB_FLAG_OFF(def_done), t - 1,
                  c.mode != SPLIT && t >= 2);
         Flags* f = flags_of(c, c.r);
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // this stream; else from a forward (batch t), after it
         const uint32_t tt = (flag_arg & 16) ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, tt);
+        EMB_TR_WAITED(10 + kind, tt);
         if (flag_arg & 1) publish(c, EMB_FLAG_OFF(ids), tt);
         if (flag_arg & 2) wait_all(c, flags_of(c, c.r)->ids, tt, 4);
         // (the scheduled merge reads the merge plan, not the routing tables, so
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // gate completed; every sender's pass must have completed
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
+        EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
         const int part = (kind == GATE_PUB1) ? 1 : 0;
         if (!part) st_release_gpu(c.seq + SEQ_APPLIED, t);     // the apply of t completed (side stream waits)
         else st_release_gpu(c.seq + SEQ_DEFPUSHED, t);          // defpush(t) no longer needs the routing tables
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // apply of t (SPLIT): the D_next tags of t+1 are complete (mark, aux stream)
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
+        EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
         wait_local(c, c.marked + p, t, 8 * 16);
         EMB_TR_END(10 + kind, t);
         break;
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // N == 1 also the prefetch check (fingerprints of fwd(t) and sort(t))
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
+        EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
         wait_local(c, c.sort_count + p, (t + 1) / 2, 9 * 16);  // one sort of parity p per iteration
         unsigned* f = c.fp + p * 4;
         if (f[0] != f[2] || f[1] != f[3]) atomicOr(c.err, ERR_STATE);
@@ -109,6 +114,7 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
         // the scheduled merge of t (this stream's predecessor) completed
         const uint32_t t = c.t_rec[p];
         EMB_TR_BEGIN(10 + kind, t);
+        EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
         publish(c, EMB_FLAG_OFF(def_done), t);
         EMB_TR_END(10 + kind, t);
         break;

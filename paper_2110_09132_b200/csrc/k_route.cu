@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
   const uint32_t t = t_mode ? c.side_it[0] + 1 : __ldcg(c.sorted + p);
   (void)t;
   EMB_TR_BEGIN(2, t);
+  EMB_TR_WAITED(2, t);
   const int s = blockIdx.x % c.N, k = blockIdx.x / c.N;
   int* dst = gids_of(c, s, p ^ 1, c.r);
   const int stride = MP_SLICES * MP_THREADS;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, in
   pdl_wait();
   const uint32_t t = t_mode ? __ldcg(c.side_it) : __ldcg(c.sorted + p);  // see markpush
   EMB_TR_BEGIN(17, t);
+  EMB_TR_WAITED(17, t);
   if (blockIdx.x == 0 && threadIdx.x < 2) c.plan_cnt[p * 2 + threadIdx.x] = 0;  // re-arm the plan of parity p
   if (do_mark) {
     int* mark = c.nextmark + (size_t)p * c.L;
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
   pdl_wait();
   const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   EMB_TR_BEGIN(19, t);
+  EMB_TR_WAITED(19, t);
   int cnt[EMB_WMAX];
   int total = 0;
 #pragma unroll
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p, 
   const unsigned lt_mask = (1u << lane) - 1u;
   const uint32_t t = t_mode ? __ldcg(c.side_it) : __ldcg(c.sorted + p);  // see markpush
   EMB_TR_BEGIN(9, t);
+  EMB_TR_WAITED(9, t);
   const int U = counts_of(c, p, n)[CNT_U];
   const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
   const int* uid = c.uid + bpn;

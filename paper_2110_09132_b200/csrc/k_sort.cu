@@ -105,8 +105,12 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   // (from_bwd == 2, N == 1: the sorts of consecutive batches run on two
   // streams and may overlap; only the completion count is published, the
   // epoch is not needed — no slotmap at N == 1)
-  const uint32_t tt = from_bwd == 2 ? 0u : from_bwd ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
+  // (from_bwd == 2: tt only labels the kernel trace — the sorts of parity p
+  // run in order on one stream, the next is the (count+1)-th: t = 2(count+1) - p)
+  const uint32_t tt = from_bwd == 2 ? 2u * (__ldcg(c.sort_count + p) + 1u) - (uint32_t)(p & 1)
+                      : from_bwd ? __ldcg(c.sorted + (p ^ 1)) + 1 : c.t_rec[p ^ 1] + 1;
   EMB_TR_BEGIN(1, tt);
+  EMB_TR_WAITED(1, tt);
   // N > 1: the gate before this kernel published / waited the ids flags.
   // own_ids (N == 1 prefetch): this rank's batch is read straight from the caller.
   const bool own = own_ids != nullptr && n == c.r;

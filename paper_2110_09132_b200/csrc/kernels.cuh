@@ -5,7 +5,8 @@
 namespace emb {
 
 struct LaunchCfg {
-  int nsm;  // SM count of the device
+  int nsm;         // SM count of the device
+  int fwd_per_sm;  // forward grid cap, CTAs per SM (env EMB_FWD_GRID_PER_SM, default 4)
 };
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
