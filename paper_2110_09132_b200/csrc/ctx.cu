@@ -116,7 +116,7 @@ struct emb_ctx {
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
   cudaStream_t aux2 = nullptr;  // N == 1: the sorts of odd batches (two sorts may overlap; 8 SMs each)
-  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {};
+  cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {}, ev_plan[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
   bool tables_pending[2] = {false, false};  // N == 1: tables(t) on the side stream still reads parity t&1
@@ -323,6 +323,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     if (cudaEventCreateWithFlags(&ctx->ev_main[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_sorted[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaEventCreateWithFlags(&ctx->ev_tables[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+    if (cudaEventCreateWithFlags(&ctx->ev_plan[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
   }
   if (cudaEventCreateWithFlags(&ctx->ev_marked, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming) != cudaSuccess) goto fail;
@@ -482,6 +483,8 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // in the forward's last CTA instead was measured to deadlock under CUDA
   // graphs (the graph may serialise the sort behind the spinning forward;
   // profiles/r02_tune), so no spin crosses a stream here.
+  // (N > 1: the coalesce joins sort(t) instead — the forward must not wait for
+  // the aux chain, whose sort follows a cross-GPU wait; see backward)
   const bool join = pre && ctx->pl.N == 1 && ctx->sort_join && ctx->sort_pending[p];
   if (join) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
   ctx->fwd_joined = join;
@@ -551,6 +554,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // The aux / side kernels of backward(t) take t from sorted[p] (the sort of t
   // precedes them on their stream) or the side stream's own count, never from
   // t_rec (written by forward(t), which an early fork may precede).
+  // N > 1, sort(t) launched by backward(t-1) on aux: the coalesce below takes
+  // a stream dependency on it (event join) instead of a GATE_SORTED kernel
+  const bool sjoin = N > 1 && ctx->sort_join && ctx->sort_pending[p] && !ctx->fwd_joined;
   CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
   cudaEvent_t fork = early ? ctx->ev_pre : ctx->ev_main[p];
   CKC(ctx, cudaStreamWaitEvent(aux, fork, 0));
@@ -563,7 +569,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
   // serial order (profilers replay kernels one at a time).
   // (N == 1 prefetched: the forward already joined the sort's event — the
   // coalesce checks the prefetch fingerprints in its CTA 0.)
-  if (!ctx->fwd_joined)
+  if (sjoin)
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
+  else if (!ctx->fwd_joined)
     CKC(ctx, run_k(ctx, EMB_K_GATE, stream, [&] { return launch_gate(ctx->dc, p, GATE_SORTED, 0, stream); }));
 
   if (N == 1) {
@@ -616,6 +624,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, next_ids ? (1 | 2 | 4 | 8 | 16) : (8 | 16), aux));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, 0, aux); }));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
+    CKC(ctx, cudaEventRecord(ctx->ev_plan[p], aux));  // D_next tags + merge plan of t complete
     ctx->aux_used = true;
     if (next_ids) {
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
@@ -639,7 +648,12 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // aux-stream kernel that sets it — timeouts)
     const int cg = (N == 1 ? 1 : 0);
     CKC(ctx, run_k(ctx, EMB_K_COAL, stream, [&] { return launch_coal(c, lc, grad_out, p, cg, stream); }));
-    if (mode == EMB_BWD_SPLIT) CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
+    // N > 1 SPLIT: the apply routes by the D_next tags of t+1 (aux, launched
+    // above in this call): an event join, or the GATE_MARKED spin kernel
+    if (mode == EMB_BWD_SPLIT && N > 1) {
+      if (ctx->sort_join) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_plan[p], 0));
+      else CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
+    }
     CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.
@@ -923,6 +937,7 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_main[i]) cudaEventDestroy(ctx->ev_main[i]);
     if (ctx->ev_sorted[i]) cudaEventDestroy(ctx->ev_sorted[i]);
     if (ctx->ev_tables[i]) cudaEventDestroy(ctx->ev_tables[i]);
+    if (ctx->ev_plan[i]) cudaEventDestroy(ctx->ev_plan[i]);
   }
   for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre, ctx->ev_join_aux2}) {
     if (e) cudaEventDestroy(e);
