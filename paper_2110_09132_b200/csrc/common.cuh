@@ -92,6 +92,7 @@ struct DevCtx {
   unsigned int* seq;      // [4]   progress records: [SEQ_BWD] t past the sort gate, [SEQ_APPLIED] t past the
                           //       apply, [SEQ_DEFPUSHED] t past the scheduled push (the sort of t+2 waits it)
   unsigned int* fwd_dd;   // [2]   N > 1: the forward of parity p dedups (sort(t) was already complete at its gate)
+  unsigned int* merge_cnt;  // [2] N > 1: CTAs of the running merge(part 0) of parity p that finished
   unsigned int* fp;       // [2][4] N == 1 prefetch check: {sum h(ids fwd), n fwd, sum h(next_ids sort), n sort}
   float* alpha;           // [2]   Adam step size alpha_t (computed once by the forward)
   int* err;               // sticky error bits

@@ -296,6 +296,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.mark_cnt, 2 * 4);
     ALLOC(c.seq, 4 * 4);
     ALLOC(c.fwd_dd, 2 * 4);
+    ALLOC(c.merge_cnt, 2 * 4);
     ALLOC(c.fp, 2 * 4 * 4);
     ALLOC(c.alpha, 2 * 4);
     ALLOC(c.err, 4);
@@ -623,8 +624,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     if (next_ids) CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, 0, aux); }));
     CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, next_ids ? (1 | 2 | 4 | 8 | 16) : (8 | 16), aux));
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, 0, aux); }));
+    CKC(ctx, cudaEventRecord(ctx->ev_plan[p], aux));  // D_next tags of t+1 complete (the apply routes by them)
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
-    CKC(ctx, cudaEventRecord(ctx->ev_plan[p], aux));  // D_next tags + merge plan of t complete
     ctx->aux_used = true;
     if (next_ids) {
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
@@ -633,7 +634,9 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], aux));
       ctx->sort_pending[p ^ 1] = true;
     }
-    CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, 0, aux); }));
+    // the Alg. 1 slot tables of t (presentation: stats / debug) stay off the
+    // aux chain in SPLIT (side stream, after the scheduled push: see below)
+    if (mode != EMB_BWD_SPLIT) CKC(ctx, run_k(ctx, EMB_K_TABLES, aux, [&] { return launch_tables(c, p, 0, aux); }));
   }
   ctx->sort_pending[p] = false;
   if (mode == EMB_BWD_RAW) {
@@ -669,6 +672,10 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, cudaStreamWaitEvent(side, ctx->ev_prior[p], 0));
       if (ctx->pl.N > 1)  // N == 1: coal wrote every row to its receive slot directly
         CKC(ctx, run_k(ctx, EMB_K_DEFPUSH, side, [&] { return launch_defpush(c, lc, p, side); }));
+      // tables(t) reads sort(t)'s unique lists and the D_next tags of t+1 (both
+      // complete: the apply joined them); GATE_PUB1 then records SEQ_DEFPUSHED,
+      // which the sort of t+2 waits for before it rewrites the lists
+      CKC(ctx, run_k(ctx, EMB_K_TABLES, side, [&] { return launch_tables(c, p, 0, side); }));
       CKC(ctx, gate(ctx, p, GATE_PUB1, 0, side));
       CKC(ctx, run_k(ctx, EMB_K_MERGE1, side, [&] { return launch_merge(c, lc, p, 1, side); }));
       CKC(ctx, gate(ctx, p, GATE_DEFDONE, 0, side));  // def_done(t) to every owner

@@ -628,6 +628,23 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       st16(wp, Vec<DT>::pack(w));
     }
   }
+  if (part == 0 && c.N > 1) {
+    // the LAST CTA to finish announces prior_done(t) (and, outside SPLIT,
+    // def_done(t): there is no second part) to every owner: the next forward's
+    // gate then only waits, and the flag leaves as soon as the update is
+    // complete instead of after the next gate kernel's own dependency wait
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(c.merge_cnt + p, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      c.merge_cnt[p] = 0;
+      publish2(c, EMB_FLAG_OFF(prior_done), t, true, EMB_FLAG_OFF(def_done), t, c.mode != SPLIT);
+    }
+  }
   EMB_TR_END(part ? 6 : 4, t);
   pdl_trigger();
 }

@@ -29,14 +29,13 @@ __global__ void __launch_bounds__(32) gate_kernel(DevCtx c, int p, int kind, int
   if (threadIdx.x == 0) {
     switch (kind) {
       case GATE_FWD: {
-        // forward(t): the main stream completed merge(prior, t-1): publish it;
-        // SPLIT: def_done(t-2) comes from GATE_DEFDONE on the side stream.  Every
-        // owner (this rank included) must have applied both parts.
+        // forward(t): every owner (this rank included) must have applied the
+        // prior part of t-1 (published by the last CTA of its merge(part 0),
+        // k_bwd.cu) and the scheduled part of t-2 (SPLIT: GATE_DEFDONE on its
+        // side stream; otherwise with prior_done)
         const uint32_t t = c.t_rec[p ^ 1] + 1;
         EMB_TR_BEGIN(10 + kind, t);
         EMB_TR_WAITED(10 + kind, t);  // past griddepcontrol.wait (predecessor complete)
-        publish2(c, EMB_FLAG_OFF(prior_done), t - 1, t >= 2, EMB_FLAG_OFF(def_done), t - 1,
-                 c.mode != SPLIT && t >= 2);
         Flags* f = flags_of(c, c.r);
         wait_all(c, f->prior_done, t - 1, 1);
         wait_all(c, f->def_done, t - 2, 2);

@@ -178,9 +178,23 @@ __global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
         }
       }
     }
-    if (!leader) continue;
     const int part = (c.mode == SPLIT && !is_prior(c, p, t, u)) ? 1 : 0;
-    const int slot = atomicAdd(&c.plan_cnt[p * 2 + part], 1);
+    // warp-aggregated slot allocation: one atomic per (warp, part), not per entry
+    // (the order of plan entries is free: every entry is one id's whole merge)
+    const unsigned act = __activemask();
+    const unsigned m1 = __ballot_sync(act, leader && part == 1), m0 = __ballot_sync(act, leader && part == 0);
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int base0 = 0, base1 = 0;
+    const int first = __ffs(act) - 1;
+    if (lane == first) {
+      if (m0) base0 = atomicAdd(&c.plan_cnt[p * 2 + 0], __popc(m0));
+      if (m1) base1 = atomicAdd(&c.plan_cnt[p * 2 + 1], __popc(m1));
+    }
+    base0 = __shfl_sync(act, base0, first);
+    base1 = __shfl_sync(act, base1, first);
+    if (!leader) continue;
+    const int slot = part ? base1 + __popc(m1 & lt) : base0 + __popc(m0 & lt);
     int* e = c.plan + (((size_t)p * 2 + part) * c.N * c.max_tok + slot) * PW;
     e[0] = u;
 #pragma unroll
