@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="lstm_lm")
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
+    ap.add_argument("--optim", default=None, choices=["sgd", "adam", "adagrad"],
+                    help="override the config's sparse optimizer (NEXT-4: adagrad)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--graph-no-prefetch", action="store_true",
@@ -172,7 +174,7 @@ def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
     out["mark_next"] = (T[rank] * 4 * (N + 1) + (sum(T) * 8 if mode == "split" else 0), (N - 1) * T[rank] * 4)
     out["sort_unique"] = (sum(T) * 4 * 3 + sum(u) * 4 * 4 + (sum(u) * 8 if N > 1 else 0), 0)
     out["split_tables"] = (sum(u) * 4 * 3, 0)
-    opt_b = 16 if cfg.optim == "adam" else 0   # Adam m, v fp32: read + write
+    opt_b = {"adam": 16, "adagrad": 8}.get(cfg.optim, 0)   # Adam m, v / Adagrad accumulator, fp32: read + write
     row_state = 2 * esz + opt_b               # shard row element read + write (+ m, v)
     if mode == "raw":
         out["rawpush"] = (T[rank] * cfg.D * esz * 2, (N - 1) * T[rank] * d * esz)
@@ -453,6 +455,9 @@ def main():
     if world != args.gpus:
         world = args.gpus if world == 1 else world
     cfg = get_config(args.config)
+    if args.optim:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, optim=args.optim, lr=cfg.lr if args.optim == "adam" else 1e-2)
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
     if args.dense_queue:

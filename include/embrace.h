@@ -64,7 +64,11 @@ typedef enum {
 } emb_status;
 
 typedef enum { EMB_FP32 = 0, EMB_BF16 = 1 } emb_dtype; /* table, wire and output dtype */
-typedef enum { EMB_SGD = 0, EMB_ADAM = 1 } emb_optim;
+/* Sparse optimizers (reading R4).  EMB_ADAGRAD (SURVEY
+ * §8(f) NEXT-4; "common sparse optimizer such as Adagrad"):
+ * PyTorch Adagrad with lr_decay 0 and initial accumulator 0, s += g^2,
+ * w -= lr g / (sqrt(s) + eps); its accumulator is EMB_STATE_ADAM_M.        */
+typedef enum { EMB_SGD = 0, EMB_ADAM = 1, EMB_ADAGRAD = 2 } emb_optim;
 /* Backward modes (reading R2):
  *   RAW   — plain hybrid communication: uncoalesced dY column slices travel,
  *           the owner coalesces;
@@ -141,7 +145,7 @@ typedef enum {
                              waited, finished, phase stamps] globaltimer ns (EMB_TRACE builds) */
 } emb_debug_item;
 
-typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1, EMB_STATE_ADAM_V = 2 } emb_state_item;
+typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1 /* Adagrad: accumulator */, EMB_STATE_ADAM_V = 2 } emb_state_item;
 
 typedef struct emb_ctx emb_ctx;
 

@@ -45,7 +45,7 @@ from .bf16 import round_to
 
 @dataclass
 class OptimConfig:
-    kind: str = "sgd"            # "sgd" | "adam"
+    kind: str = "sgd"            # "sgd" | "adam" | "adagrad" (the accumulator rides in m)
     lr: float = 0.1
     beta1: float = 0.9
     beta2: float = 0.999
@@ -218,6 +218,8 @@ def simulate_iteration(shards, ids, dY, next_ids, t, mode="split", dtype="fp32",
             old_W = np.asarray(shards[r][rows], np.float64)
             if opt.kind == "sgd":
                 optim.sgd_apply(shards[r], rows, g_r, opt.lr, store=dtype)
+            elif opt.kind == "adagrad":
+                optim.adagrad_apply(shards[r], m[r], rows, g_r, opt.lr, opt.eps, store=dtype, sstore="fp32")
             else:
                 optim.adam_apply(shards[r], m[r], v[r], rows, g_r, t, opt.lr, opt.beta1, opt.beta2,
                                  opt.eps, store=dtype, mstore="fp32")
@@ -227,6 +229,11 @@ def simulate_iteration(shards, ids, dY, next_ids, t, mode="split", dtype="fp32",
             res.sigma_g[at, c0:c1] = sg_r
             if opt.kind == "sgd":
                 res.sigma_W[at, c0:c1] = np.abs(old_W) + opt.lr * sg_r
+            elif opt.kind == "adagrad":
+                res.sigma_W[at, c0:c1] = np.abs(old_W) + np.abs(new_W - old_W)
+                # accumulator s += g^2: first-order magnitude |s| + 2 |g| sigma_g
+                res.sigma_m[at, c0:c1] = (np.abs(np.asarray(m[r][rows], np.float64))
+                                          + 2 * np.abs(g_r) * sg_r)
             else:
                 res.sigma_W[at, c0:c1] = np.abs(old_W) + np.abs(new_W - old_W)
                 res.sigma_m[at, c0:c1] = np.abs(np.asarray(m[r][rows], np.float64)) + (1 - opt.beta1) * sg_r
@@ -272,6 +279,8 @@ def dense_reference(W, ids, dY, t, dtype="fp32", opt=None, m=None, v=None, pad_i
     g = scale * G[U]
     if opt.kind == "sgd":
         optim.sgd_apply(W, U, g, opt.lr, store=dtype)
+    elif opt.kind == "adagrad":
+        optim.adagrad_apply(W, m, U, g, opt.lr, opt.eps, store=dtype, sstore="fp32")
     else:
         optim.adam_apply(W, m, v, U, g, t, opt.lr, opt.beta1, opt.beta2, opt.eps,
                          store=dtype, mstore="fp32")

@@ -66,6 +66,23 @@ def adam_apply(W, m, v, idx, g, t, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
     W[idx] = round_to(W_new, store)
 
 
+def adagrad_apply(W, s, idx, g, lr=1e-2, eps=1e-10, store="fp64", sstore="fp64"):
+    """One sparse Adagrad update of rows ``idx`` (PAPER.md:594
+    "the common sparse optimizer such as Adagrad [...] is fully element-wise";
+    PyTorch Adagrad form, lr_decay 0, initial accumulator 0):
+        s <- s + g^2
+        W <- W - lr * g / (sqrt(s) + eps)
+    Element-wise: updating disjoint row parts separately equals one update."""
+    idx = np.asarray(idx, dtype=np.int64)
+    if idx.size == 0:
+        return
+    g = np.asarray(g, np.float64)
+    s_new = np.asarray(s[idx], np.float64) + g * g
+    W_new = np.asarray(W[idx], np.float64) - lr * g / (np.sqrt(s_new) + eps)
+    s[idx] = round_to(s_new, sstore)
+    W[idx] = round_to(W_new, store)
+
+
 class PartialAdam:
     """The paper's modified Adam under reading R3: the step value
     of iteration k is t = committed + 1 for every part of that iteration; the

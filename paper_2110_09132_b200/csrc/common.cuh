@@ -12,7 +12,7 @@
 namespace emb {
 
 enum Mode { RAW = 0, COAL = 1, SPLIT = 2 };
-enum Optim { SGD = 0, ADAM = 1 };
+enum Optim { SGD = 0, ADAM = 1, ADAGRAD = 2 };
 enum DType { F32 = 0, BF16 = 1 };
 enum ErrBit { ERR_ID = 1, ERR_STATE = 2, ERR_TIMEOUT = 4 };
 // counts[p][n][CNT_W]
@@ -63,7 +63,7 @@ struct DevCtx {
   SymLayout lay;
 
   // local (not peer-visible); [2] = iteration parity p = t & 1
-  float* adam_m;          // [L][d]
+  float* adam_m;          // [L][d]   Adam first moment; Adagrad: the squared-gradient accumulator
   float* adam_v;          // [L][d]
   int* nextmark;          // [2][L]   epoch tag: id in D_next of iteration v <=> nextmark[v&1][id] == v+1
   unsigned long long* slotmap;  // [2][L][N] (t << 32) | i — source n holds id as unique i at iteration t (N > 1)

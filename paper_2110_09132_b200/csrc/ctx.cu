@@ -53,7 +53,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (cfg->dim < 1 || cfg->max_tokens < 1 || cfg->max_tokens > 16384) return EMB_ERR_CAPACITY;
   if (cfg->dtype != EMB_FP32 && cfg->dtype != EMB_BF16) return EMB_ERR_INVALID_ARG;
   if (cfg->mode < EMB_BWD_RAW || cfg->mode > EMB_BWD_SPLIT) return EMB_ERR_INVALID_ARG;
-  if (cfg->optim != EMB_SGD && cfg->optim != EMB_ADAM) return EMB_ERR_INVALID_ARG;
+  if (cfg->optim != EMB_SGD && cfg->optim != EMB_ADAM && cfg->optim != EMB_ADAGRAD) return EMB_ERR_INVALID_ARG;
   if (cfg->queue_window < 0) return EMB_ERR_INVALID_ARG;
   const int N = cfg->world;
   if (N > cfg->dim || cfg->dim % N != 0) return EMB_ERR_SHAPE;
@@ -86,6 +86,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
 
   size_t loc = 0;
   if (cfg->optim == EMB_ADAM) loc += 2 * L * pl->d * 4;
+  if (cfg->optim == EMB_ADAGRAD) loc += L * pl->d * 4;
   if (N > 1) loc += 2 * L * N * 8;                               // slotmap
   loc += 2 * L * 4;                                              // nextmark
   loc += 3 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id | useg chunk_off
@@ -249,7 +250,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   memset(&c, 0, sizeof(c));
   c.N = pl.N; c.r = pl.r; c.L = cfg->vocab; c.D = cfg->dim; c.d = pl.d; c.esz = pl.esz;
   c.dtype = cfg->dtype == EMB_BF16 ? BF16 : F32;
-  c.mode = (int)cfg->mode; c.optim = cfg->optim == EMB_ADAM ? ADAM : SGD;
+  c.mode = (int)cfg->mode; c.optim = cfg->optim == EMB_ADAM ? ADAM : (cfg->optim == EMB_ADAGRAD ? ADAGRAD : SGD);
   c.max_tok = cfg->max_tokens; c.cpr = pl.cpr; c.cps = pl.cps; c.pad_id = cfg->pad_id;
   c.lr = cfg->lr; c.beta1 = cfg->beta1; c.beta2 = cfg->beta2; c.eps = cfg->eps;
   c.scale = cfg->grad_scale != 0.f ? cfg->grad_scale : 1.0f / (float)pl.N;
@@ -271,6 +272,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
       ALLOC(c.adam_m, L * pl.d * 4);
       ALLOC(c.adam_v, L * pl.d * 4);
     }
+    if (cfg->optim == EMB_ADAGRAD) ALLOC(c.adam_m, L * pl.d * 4);  // the accumulator
     if (N > 1) ALLOC(c.slotmap, 2 * L * N * 8);
     ALLOC(c.nextmark, 2 * L * 4);
     ALLOC(c.perm, 2 * N * T * 4);
@@ -376,10 +378,8 @@ __global__ void boot_kernel(DevCtx c, uint32_t val) {
 static emb_status shard_load(emb_ctx* ctx, const void* shard_init, cudaStream_t stream) {
   const size_t shard_bytes = (size_t)ctx->cfg.vocab * ctx->pl.d * ctx->pl.esz;
   CKC(ctx, cudaMemcpyAsync(ctx->sym + ctx->pl.lay.shard, shard_init, shard_bytes, cudaMemcpyDeviceToDevice, stream));
-  if (ctx->dc.adam_m) {
-    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_m, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
-    CKC(ctx, cudaMemsetAsync(ctx->dc.adam_v, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
-  }
+  if (ctx->dc.adam_m) CKC(ctx, cudaMemsetAsync(ctx->dc.adam_m, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
+  if (ctx->dc.adam_v) CKC(ctx, cudaMemsetAsync(ctx->dc.adam_v, 0, (size_t)ctx->cfg.vocab * ctx->pl.d * 4, stream));
   boot_kernel<<<1, 32, 0, stream>>>(ctx->dc, 1u);
   CKC(ctx, cudaGetLastError());
   return EMB_OK;

@@ -159,14 +159,26 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Sparse optimizer math on EPV elements of one row chunk; g = merged, unscaled
 // gradient.  SGD: w -= lr*g.  Adam (PyTorch SparseAdam form, step t folded
 // into alpha_t, readings R3/R4): m += (1-b1)(g-m); v += (1-b2)(g^2-v);
-// w -= alpha_t m / (sqrt(v)+eps).  sqrt / reciprocal use the SFU (MUFU)
-// approximations: relative error ~1e-7, far inside the 1e-5 parity bound,
-// where an IEEE div+sqrt would cost ~30 instructions per element.
+// w -= alpha_t m / (sqrt(v)+eps).  Adagrad (PAPER.md:594
+// names it among the element-wise sparse optimizers; PyTorch Adagrad form with
+// lr_decay 0, initial accumulator 0): s += g^2; w -= lr g / (sqrt(s)+eps), the
+// accumulator s kept in the first-moment buffer.  sqrt / reciprocal use the
+// SFU (MUFU) approximations: relative error ~1e-7, far inside the 1e-5 parity
+// bound, where an IEEE div+sqrt would cost ~30 instructions per element.
 template <int EPV>
 __device__ __forceinline__ void opt_math(const DevCtx& c, float alpha, const float* g, float* w, float* mm, float* vv) {
   if (c.optim == SGD) {
 #pragma unroll
     for (int i = 0; i < EPV; ++i) w[i] = w[i] - c.lr * (c.scale * g[i]);
+    return;
+  }
+  if (c.optim == ADAGRAD) {
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) {
+      const float gs = c.scale * g[i];
+      mm[i] = mm[i] + gs * gs;
+      w[i] = w[i] - c.lr * gs * rcp_approx(sqrt_approx(mm[i]) + c.eps);
+    }
     return;
   }
   const float om_b1 = 1.f - c.beta1, om_b2 = 1.f - c.beta2;
@@ -262,13 +274,15 @@ __device__ __forceinline__ void apply_load(const DevCtx& c, int id, int c16, App
   if (c.N != 1) return;
   const size_t u = (size_t)id;
   st.w = ld16(shard_of(c, c.r) + u * ((size_t)c.d * c.esz) + (size_t)c16 * 16);
-  if (c.optim == ADAM) {
+  if (c.optim != SGD) {  // Adam m, v; Adagrad accumulator (in m)
 #pragma unroll
     for (int x = 0; x < EPV; x += 4) {
       const float4 m4 = *reinterpret_cast<const float4*>(c.adam_m + u * c.d + c16 * EPV + x);
-      const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + c16 * EPV + x);
       st.m[x] = m4.x; st.m[x + 1] = m4.y; st.m[x + 2] = m4.z; st.m[x + 3] = m4.w;
-      st.v[x] = v4.x; st.v[x + 1] = v4.y; st.v[x + 2] = v4.z; st.v[x + 3] = v4.w;
+      if (c.optim == ADAM) {
+        const float4 v4 = *reinterpret_cast<const float4*>(c.adam_v + u * c.d + c16 * EPV + x);
+        st.v[x] = v4.x; st.v[x + 1] = v4.y; st.v[x + 2] = v4.z; st.v[x + 3] = v4.w;
+      }
     }
   }
 }
@@ -285,13 +299,14 @@ __device__ __forceinline__ void apply_store(const DevCtx& c, int p, uint32_t t, 
     Vec<DT>::unpack(st.w, wv);
     opt_math<EPV>(c, alpha, gr, wv, st.m, st.v);
     st16(shard_of(c, c.r) + u * slice_bytes + (size_t)c16 * 16, Vec<DT>::pack(wv));
-    if (c.optim == ADAM) {
+    if (c.optim != SGD) {
 #pragma unroll
       for (int x = 0; x < EPV; x += 4) {
         *reinterpret_cast<float4*>(c.adam_m + u * c.d + c16 * EPV + x) =
             make_float4(st.m[x], st.m[x + 1], st.m[x + 2], st.m[x + 3]);
-        *reinterpret_cast<float4*>(c.adam_v + u * c.d + c16 * EPV + x) =
-            make_float4(st.v[x], st.v[x + 1], st.v[x + 2], st.v[x + 3]);
+        if (c.optim == ADAM)
+          *reinterpret_cast<float4*>(c.adam_v + u * c.d + c16 * EPV + x) =
+              make_float4(st.v[x], st.v[x + 1], st.v[x + 2], st.v[x + 3]);
       }
     }
   } else if (is_prior(c, p, t, id)) {
@@ -584,13 +599,15 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       float mm[EPV], vv[EPV];
       float* mp = c.adam_m + (size_t)u * c.d + c16 * EPV;
       float* vp = c.adam_v + (size_t)u * c.d + c16 * EPV;
-      if (c.optim == ADAM) {
+      if (c.optim != SGD) {
 #pragma unroll
         for (int i = 0; i < EPV; i += 4) {
           const float4 m4 = *reinterpret_cast<const float4*>(mp + i);
-          const float4 v4 = *reinterpret_cast<const float4*>(vp + i);
           mm[i] = m4.x; mm[i + 1] = m4.y; mm[i + 2] = m4.z; mm[i + 3] = m4.w;
-          vv[i] = v4.x; vv[i + 1] = v4.y; vv[i + 2] = v4.z; vv[i + 3] = v4.w;
+          if (c.optim == ADAM) {
+            const float4 v4 = *reinterpret_cast<const float4*>(vp + i);
+            vv[i] = v4.x; vv[i + 1] = v4.y; vv[i + 2] = v4.z; vv[i + 3] = v4.w;
+          }
         }
       }
       float g[EPV];
@@ -618,11 +635,12 @@ __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int
       float w[EPV];
       Vec<DT>::unpack(wraw, w);
       opt_math<EPV>(c, alpha, g, w, mm, vv);
-      if (c.optim == ADAM) {
+      if (c.optim != SGD) {
 #pragma unroll
         for (int i = 0; i < EPV; i += 4) {
           *reinterpret_cast<float4*>(mp + i) = make_float4(mm[i], mm[i + 1], mm[i + 2], mm[i + 3]);
-          *reinterpret_cast<float4*>(vp + i) = make_float4(vv[i], vv[i + 1], vv[i + 2], vv[i + 3]);
+          if (c.optim == ADAM)
+            *reinterpret_cast<float4*>(vp + i) = make_float4(vv[i], vv[i + 1], vv[i + 2], vv[i + 3]);
         }
       }
       st16(wp, Vec<DT>::pack(w));

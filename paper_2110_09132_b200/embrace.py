@@ -22,7 +22,8 @@ STATUS = {0: "EMB_OK", 1: "EMB_ERR_INVALID_ARG", 2: "EMB_ERR_SHAPE", 3: "EMB_ERR
           4: "EMB_ERR_CAPACITY", 5: "EMB_ERR_STATE", 6: "EMB_ERR_CUDA", 7: "EMB_ERR_NCCL",
           8: "EMB_ERR_TIMEOUT"}
 EMB_FP32, EMB_BF16 = 0, 1
-EMB_SGD, EMB_ADAM = 0, 1
+EMB_SGD, EMB_ADAM, EMB_ADAGRAD = 0, 1, 2
+OPTIMS = {"sgd": EMB_SGD, "adam": EMB_ADAM, "adagrad": EMB_ADAGRAD}
 EMB_BWD_RAW, EMB_BWD_COAL, EMB_BWD_SPLIT = 0, 1, 2
 EMB_DBG_GIDS, EMB_DBG_SLOT_IDS, EMB_DBG_COUNTS, EMB_DBG_PERM, EMB_DBG_ISSUE_LOG, EMB_DBG_TIMESTAMPS, \
     EMB_DBG_ERRINFO = range(7)
@@ -140,7 +141,7 @@ def make_config(vocab, dim, world=1, rank=0, device=0, dtype="fp32", max_tokens=
                 optim="sgd", lr=0.1, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale=0.0, pad_id=-1,
                 queue_window=1, timeout_ms=10000):
     return EmbConfig(vocab, dim, world, rank, device, EMB_BF16 if dtype == "bf16" else EMB_FP32, max_tokens,
-                     MODES[mode] if isinstance(mode, str) else mode, EMB_ADAM if optim == "adam" else EMB_SGD,
+                     MODES[mode] if isinstance(mode, str) else mode, OPTIMS[optim],
                      lr, beta1, beta2, eps, grad_scale, pad_id, queue_window, timeout_ms)
 
 

@@ -118,7 +118,7 @@ def _gather_state(rk, rows, optim):
         dev = ex.shard().device
         idx = torch.from_numpy(rows).to(dev)
         gW = _np64(ex.shard()[idx]) if rows.size else None
-        gm = _np64(ex.adam_m()[idx]) if (optim == "adam" and rows.size) else None
+        gm = _np64(ex.adam_m()[idx]) if (optim in ("adam", "adagrad") and rows.size) else None
         gv = _np64(ex.adam_v()[idx]) if (optim == "adam" and rows.size) else None
         out.append((r, gW, gm, gv))
     if rk.N > 1 and not rk.colocated:
@@ -152,7 +152,7 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
     W = gen_table(cfg)
     shards = partition.partition_columnwise(W, N)                     # oracle state (float32 grid values)
     del W
-    m = [np.zeros_like(s) for s in shards] if optim == "adam" else None
+    m = [np.zeros_like(s) for s in shards] if optim in ("adam", "adagrad") else None   # adagrad: accumulator
     v = [np.zeros_like(s) for s in shards] if optim == "adam" else None
     opt = exchange.OptimConfig(optim, lr=lr)
     d = cfg.D // N
@@ -246,11 +246,12 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
                     if cfg.dtype == "bf16":
                         errs["dW_ulp"] = max(errs["dW_ulp"], assert_update(gW, shards[r][rows], old[r],
                                                                            f"iter {t} rank {r} bf16 update"))
-                if optim == "adam":
-                    sm = acc["m"].get(rows)[:, c0:c1] if free else res.sigma_m[:, c0:c1]
-                    sv = acc["v"].get(rows)[:, c0:c1] if free else res.sigma_v[:, c0:c1]
+                if optim in ("adam", "adagrad"):
                     f = assert_close_acc if free else assert_close
-                    errs["m"] = max(errs["m"], f(gm, m[r][rows], sm, cfg.dtype, f"iter {t} rank {r} adam m"))
+                    sm = acc["m"].get(rows)[:, c0:c1] if free else res.sigma_m[:, c0:c1]
+                    errs["m"] = max(errs["m"], f(gm, m[r][rows], sm, cfg.dtype, f"iter {t} rank {r} {optim} m"))
+                if optim == "adam":
+                    sv = acc["v"].get(rows)[:, c0:c1] if free else res.sigma_v[:, c0:c1]
                     errs["v"] = max(errs["v"], f(gv, v[r][rows], sv, cfg.dtype, f"iter {t} rank {r} adam v"))
             # rows outside U are bit-identical (sampled)
             rng = np.random.default_rng(t)
@@ -270,6 +271,7 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
                         shards[r][rows] = gW
                         if gm is not None:
                             m[r][rows] = gm
+                        if gv is not None:
                             v[r][rows] = gv
         if pipelined and check:
             rk.flush()
@@ -287,9 +289,10 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
                 c0, c1 = r * d, (r + 1) * d
                 errs["W"] = max(errs["W"], assert_close_acc(gW, shards[r][rows], acc["W"].get(rows)[:, c0:c1],
                                                             cfg.dtype, f"pipelined final rank {r} shard"))
-                if optim == "adam":
+                if optim in ("adam", "adagrad"):
                     errs["m"] = max(errs["m"], assert_close_acc(gm, m[r][rows], acc["m"].get(rows)[:, c0:c1],
                                                                 cfg.dtype, f"pipelined final rank {r} m"))
+                if optim == "adam":
                     errs["v"] = max(errs["v"], assert_close_acc(gv, v[r][rows], acc["v"].get(rows)[:, c0:c1],
                                                                 cfg.dtype, f"pipelined final rank {r} v"))
             sample = np.setdiff1d(np.random.default_rng(7).integers(0, cfg.L, size=min(cfg.L, 4096)), rows)
@@ -308,8 +311,9 @@ def _accumulate(acc, res, optim):
     if not res.U.size:
         return
     acc["W"].add(res.U, res.sigma_W)
-    if optim == "adam":
+    if optim in ("adam", "adagrad"):
         acc["m"].add(res.U, res.sigma_m)
+    if optim == "adam":
         acc["v"].add(res.U, res.sigma_v)
 
 

@@ -89,3 +89,9 @@ def test_pipelined_paper_shape(n):
 def test_graph_replay_colocated():
     """The bench's CUDA-graph cycle, two co-located ranks, replayed twice."""
     graph_parity(_small("gnmt", 8), N=2, colocated=True)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_adagrad_colocated(n):
+    parity_run(get_config("tiny"), N=n, mode="split", iters=3, optim="adagrad", lr=0.05, colocated=True)
+    parity_run(_small("bert_large", 2), N=n, mode="split", iters=3, optim="adagrad", lr=1e-2, colocated=True)

@@ -199,3 +199,14 @@ def test_backward_null_then_forward_no_flush():
     """backward(next_ids = NULL) followed by forward without a
     flush in between must not lose the next batch's gradient."""
     parity_run(get_config("tiny"), N=1, mode="split", iters=5, null_at=(0, 1, 2), pipelined=True)
+
+
+# ---------------------------------------------------------------- NEXT-4: sparse Adagrad
+
+@pytest.mark.parametrize("mode", ["raw", "coal", "split"])
+def test_adagrad_tiny(mode):
+    parity_run(get_config("tiny"), N=1, mode=mode, iters=4, optim="adagrad", lr=0.05)
+
+
+def test_adagrad_bf16_paper_shape_free_running():
+    parity_run(_small("gnmt", batch=8), N=1, mode="split", iters=6, optim="adagrad", lr=1e-2, free=True)

@@ -336,3 +336,62 @@ def test_sgd_matches_dense_step():
     ref = W - 0.1 * dense            # a dense-gradient SGD step
     optim.sgd_apply(W, rows, g, 0.1)
     np.testing.assert_array_equal(W, ref)
+
+
+# ---------------------------------------------------------------- NEXT-4: sparse Adagrad
+
+def test_adagrad_matches_torch_adagrad_sparse():
+    """oracle.optim.adagrad_apply against torch.optim.Adagrad on sparse
+    gradients (a library routine, independent of the oracle's code)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(21)
+    L, D = 20, 6
+    W0 = rng.standard_normal((L, D))
+    p = torch.nn.Parameter(torch.tensor(W0, dtype=torch.float64))
+    opt = torch.optim.Adagrad([p], lr=5e-2, eps=1e-10)
+    W, s = W0.copy(), np.zeros((L, D))
+    for _ in range(5):
+        rows = np.unique(rng.integers(0, L, 8))
+        g = rng.standard_normal((rows.size, D))
+        p.grad = torch.sparse_coo_tensor(torch.tensor(rows[None, :]), torch.tensor(g), (L, D))
+        opt.step()
+        optim.adagrad_apply(W, s, rows, g, 5e-2, 1e-10)
+        np.testing.assert_allclose(W, p.detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
+def test_adagrad_step1_closed_form_and_parts():
+    """Step 1 from s = 0: dW = -lr g / (|g| + eps) (a sign step); two disjoint
+    parts equal one call bitwise (element-wise optimizer)."""
+    rng = np.random.default_rng(22)
+    L, D = 12, 4
+    W = rng.uniform(-1, 1, (L, D))
+    g = rng.uniform(-1, 1, (L, D))
+    rows = np.arange(L)
+    W1, s1 = W.copy(), np.zeros((L, D))
+    optim.adagrad_apply(W1, s1, rows, g, 0.1, 1e-10)
+    np.testing.assert_allclose(W1 - W, -0.1 * g / (np.abs(g) + 1e-10), rtol=1e-14)
+    W2, s2 = W.copy(), np.zeros((L, D))
+    optim.adagrad_apply(W2, s2, rows[:5], g[:5], 0.1, 1e-10)
+    optim.adagrad_apply(W2, s2, rows[5:], g[5:], 0.1, 1e-10)
+    assert np.array_equal(W1, W2) and np.array_equal(s1, s2)
+
+
+@pytest.mark.parametrize("mode", ["raw", "coal", "split"])
+def test_adagrad_exchange_equals_dense_reference(mode):
+    """The simulated N-worker exchange with Adagrad reaches the plain definition
+    (dense scatter-add, one Adagrad step on the touched rows)."""
+    from oracle import exchange, partition
+    from synthetic import get_config, make_workload
+    from synthetic.workloads import gen_table
+    cfg = get_config("tiny")
+    wl = make_workload(cfg, 2, 3)
+    W = gen_table(cfg).astype(np.float64)
+    opt = exchange.OptimConfig("adagrad", lr=0.05, eps=1e-10)
+    shards = partition.partition_columnwise(W.copy(), 2)
+    s_sh = [np.zeros_like(x) for x in shards]
+    Wd, sd = W.copy(), np.zeros_like(W)
+    for k in range(2):
+        exchange.simulate_iteration(shards, wl.ids[k], wl.dY[k], wl.ids[k + 1], k + 1, mode, "fp64", opt, s_sh, None)
+        exchange.dense_reference(Wd, wl.ids[k], wl.dY[k], k + 1, "fp64", opt, sd, None)
+    np.testing.assert_allclose(np.hstack(shards), Wd, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.hstack(s_sh), sd, rtol=1e-12, atol=1e-14)
