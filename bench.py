@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="lstm_lm")
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
+    ap.add_argument("--tables", type=int, default=1, choices=[1, 2],
+                    help="NEXT-3: exchange this many stacked tables (same shape) in one call")
     ap.add_argument("--optim", default=None, choices=["sgd", "adam", "adagrad"],
                     help="override the config's sparse optimizer (NEXT-4: adagrad)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -201,9 +203,51 @@ def algorithmic_bytes(cfg, N, rank, ids_all, next_all, mode):
     return out
 
 
+# ---------------------------------------------------------------- several tables in one exchange (NEXT-3)
+# --tables 2: the config's table twice, stacked row-wise (embrace.h num_tables):
+# table A looked up by the batch's tokens, table B by a second token stream of
+# the same shape (LM: input and softmax tables; GNMT: encoder and decoder), B's
+# ids offset by L (global row ids).  One forward + backward serves both.
+TABLES = 1
+BASE_CFG = None
+PADS = {PAD_ID}
+
+
+def stacked(cfg, tables):
+    """(sizing config, per-table row counts): L and max_tokens of the stacked exchange."""
+    global TABLES, BASE_CFG, PADS
+    TABLES, BASE_CFG = tables, cfg
+    if tables == 1:
+        return cfg, None
+    import dataclasses
+    PADS = {PAD_ID + k * cfg.L for k in range(tables)}
+    big = dataclasses.replace(cfg, L=cfg.L * tables, **({"seq_len": cfg.seq_len * tables} if cfg.packed
+                                                        else {"batch": cfg.batch * tables}))
+    return big, [cfg.L] * tables
+
+
+def gen_ids_t(cfg, b, r):
+    if TABLES == 1:
+        return gen_ids(cfg, b, r)
+    c0 = BASE_CFG
+    return np.concatenate([k * c0.L + gen_ids(c0, b + 7919 * k, r) for k in range(TABLES)]).astype(np.int32)
+
+
+def gen_table_t(cfg):
+    if TABLES == 1:
+        return gen_table(cfg)
+    W = gen_table(BASE_CFG)
+    return np.vstack([W] * TABLES)
+
+
+def count_nonpad(x):
+    x = np.asarray(x)
+    return int(sum(int((x != pid).sum()) for pid in PADS) - (len(PADS) - 1) * x.size)
+
+
 def make_batches(cfg, N, rank, nb):
-    ids = [gen_ids(cfg, b, rank) for b in range(nb)]
-    ids_all = [[gen_ids(cfg, b, s) for s in range(N)] for b in range(nb)] if N > 1 else [[x] for x in ids]
+    ids = [gen_ids_t(cfg, b, rank) for b in range(nb)]
+    ids_all = [[gen_ids_t(cfg, b, s) for s in range(N)] for b in range(nb)] if N > 1 else [[x] for x in ids]
     dY = [gen_dY(cfg, b, rank, len(ids[b])) for b in range(nb)]
     return ids, ids_all, dY
 
@@ -216,13 +260,13 @@ def oracle_step_fn(cfg, N, mode, budget_s):
     every rank (a bounded sample) and counts only those tokens."""
     from oracle import exchange, partition
     opt = exchange.OptimConfig(cfg.optim, lr=cfg.lr)
-    W = gen_table(cfg)
+    W = gen_table_t(cfg)
     shards = partition.partition_columnwise(W, N)
     del W
-    m = [np.zeros_like(s) for s in shards] if cfg.optim == "adam" else None
+    m = [np.zeros_like(s) for s in shards] if cfg.optim in ("adam", "adagrad") else None
     v = [np.zeros_like(s) for s in shards] if cfg.optim == "adam" else None
     nb = 4
-    ids = [[gen_ids(cfg, b, s) for s in range(N)] for b in range(nb)]
+    ids = [[gen_ids_t(cfg, b, s) for s in range(N)] for b in range(nb)]
     dY = [[gen_dY(cfg, b, s, len(ids[b][s])) for s in range(N)] for b in range(nb)]
     state = {"t": 0, "frac": 1.0}
 
@@ -234,7 +278,7 @@ def oracle_step_fn(cfg, N, mode, budget_s):
         nxt = [ids[(b + 1) % nb][s][: cut[s]] for s in range(N)]
         state["t"] += 1
         exchange.simulate_iteration(shards, I, G, nxt, state["t"], mode, cfg.dtype, opt, m, v)
-        return sum(int((x != PAD_ID).sum()) for x in I)
+        return sum(count_nonpad(x) for x in I)
 
     t0 = time.perf_counter()
     run(0, 1.0)
@@ -458,6 +502,7 @@ def main():
     if args.optim:
         import dataclasses
         cfg = dataclasses.replace(cfg, optim=args.optim, lr=cfg.lr if args.optim == "adam" else 1e-2)
+    cfg, table_rows = stacked(cfg, args.tables)
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
     if args.dense_queue:
@@ -480,12 +525,12 @@ def main():
     dY_d = [torch.from_numpy(x).to(dev).to(tdt) for x in dY]
     Y_d = [torch.empty((len(x), cfg.D), dtype=tdt, device=dev) for x in ids]
     d = cfg.D // world
-    W = gen_table(cfg)
+    W = gen_table_t(cfg)
     shard0 = torch.from_numpy(np.ascontiguousarray(W[:, rank * d:(rank + 1) * d])).to(dev).to(tdt)
     del W
     ex = EmbraceExchange(cfg.L, cfg.D, shard0, world=world, rank=rank, device=local, dtype=cfg.dtype,
                          max_tokens=cfg.max_tokens, mode=mode, optim=cfg.optim, lr=cfg.lr,
-                         timeout_ms=int(os.environ.get("EMB_TIMEOUT_MS", "10000")))
+                         timeout_ms=int(os.environ.get("EMB_TIMEOUT_MS", "10000")), table_rows=table_rows)
     del shard0
     stream = torch.cuda.current_stream()
 
@@ -566,7 +611,7 @@ def main():
         tt = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
-    nonpad = sum(int((np.asarray(ids_all[(k0 + j) % nb][s]) != PAD_ID).sum())
+    nonpad = sum(count_nonpad(ids_all[(k0 + j) % nb][s])
                  for j in range(K) for s in range(world))   # cycles are whole, so batch order is irrelevant
     value = nonpad / (t_max / 1e3)
 
@@ -757,7 +802,7 @@ def main():
         tt = torch.tensor([e2e_ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_tok = sum(int((np.asarray(ids_all[(kk + j) % nb][s]) != PAD_ID).sum()) for j in range(Ke) for s in range(world))
+    e2e_tok = sum(count_nonpad(ids_all[(kk + j) % nb][s]) for j in range(Ke) for s in range(world))
     check_err("end-to-end pass")
 
     # PCIe ceiling of the e2e leg: the same per-step bytes copied with no
@@ -798,7 +843,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "bf16"}[cfg.dtype], "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: L={cfg.L} D={cfg.D} {cfg.dtype} table, "
+            "config": {"workload": (f"{TABLES} stacked tables of " if TABLES > 1 else "")
+                                   + f"{cfg.name}: L={cfg.L} D={cfg.D} {cfg.dtype} table, "
                                    + (f"packed <= {cfg.seq_len} tokens" if cfg.packed else
                                       f"{cfg.batch}x{cfg.seq_len} Zipf({cfg.zipf_s}) ids") + " per rank",
                        "mode": mode, "optim": cfg.optim, "parallelism": f"column-shard x{world}",

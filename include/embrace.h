@@ -47,6 +47,7 @@ extern "C" {
 #define EMB_MAX_WORLD 8
 #define EMB_IPC_HANDLE_BYTES 64
 #define EMB_UNIQUE_ID_BYTES 128
+#define EMB_MAX_TABLES 8
 
 typedef struct CUstream_st* emb_stream_t; /* == cudaStream_t */
 typedef struct CUevent_st* emb_event_t;   /* == cudaEvent_t  */
@@ -94,6 +95,16 @@ typedef struct {
   int64_t pad_id;       /* -1: pad is an ordinary id; >= 0: its gradient is dropped */
   int32_t queue_window; /* dense queue window W >= 1 (reading R16)                  */
   int32_t timeout_ms;   /* bound on every peer-flag wait; 0 => 10000                */
+  /* Several tables in ONE exchange (PAPER.md:481 the LM's
+   * two tables, PAPER.md:319-320 GNMT's encoder and decoder tables): the tables
+   * share D and are stacked row-wise into one [vocab, D] row space, table k at
+   * rows [base_k, base_k + table_rows[k]) (emb_table_base).  A batch holding
+   * lookups of several tables passes GLOBAL row ids (local id + base_k), so one
+   * forward / backward call — one sort, one set of exchanges, one update — serves
+   * all tables; per-table outputs are row ranges of `out` / `grad_out`.
+   * num_tables = 0: one table of `vocab` rows.                               */
+  int32_t num_tables;                 /* 0 or 1..EMB_MAX_TABLES; sum(table_rows) == vocab */
+  int64_t table_rows[8];              /* EMB_MAX_TABLES                                   */
 } emb_config;
 
 typedef struct {
@@ -150,6 +161,9 @@ typedef enum { EMB_STATE_SHARD = 0, EMB_STATE_ADAM_M = 1 /* Adagrad: accumulator
 typedef struct emb_ctx emb_ctx;
 
 const char* emb_status_str(emb_status s);
+
+/* First global row of table k (num_tables > 0): sum of table_rows[0..k).     */
+emb_status emb_table_base(emb_ctx* ctx, int32_t k, int64_t* base);
 
 /* Device bytes the context will allocate (symmetric + local), for capacity
  * planning; no allocation happens.                                           */

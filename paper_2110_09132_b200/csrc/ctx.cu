@@ -55,6 +55,15 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (cfg->mode < EMB_BWD_RAW || cfg->mode > EMB_BWD_SPLIT) return EMB_ERR_INVALID_ARG;
   if (cfg->optim != EMB_SGD && cfg->optim != EMB_ADAM && cfg->optim != EMB_ADAGRAD) return EMB_ERR_INVALID_ARG;
   if (cfg->queue_window < 0) return EMB_ERR_INVALID_ARG;
+  if (cfg->num_tables < 0 || cfg->num_tables > EMB_MAX_TABLES) return EMB_ERR_INVALID_ARG;
+  if (cfg->num_tables > 0) {
+    long long sum = 0;
+    for (int k = 0; k < cfg->num_tables; ++k) {
+      if (cfg->table_rows[k] < 1) return EMB_ERR_INVALID_ARG;
+      sum += cfg->table_rows[k];
+    }
+    if (sum != cfg->vocab) return EMB_ERR_SHAPE;
+  }
   const int N = cfg->world;
   if (N > cfg->dim || cfg->dim % N != 0) return EMB_ERR_SHAPE;
   pl->N = N;
@@ -113,6 +122,7 @@ struct emb_ctx {
   bool colocated = false;  // emb_shard_init_colocated: peers are contexts of this process on this device
   bool sort_join = true;    // N == 1, prefetched: the forward waits for its sort's event (no GATE_SORTED kernel)
   bool fwd_joined = false;  // the last forward did
+  bool fwd_dedup1 = false;  // N == 1 joined forward gathers each distinct row once per chunk (knob)
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
@@ -216,6 +226,17 @@ const char* emb_status_str(emb_status s) {
   return "EMB_ERR_UNKNOWN";
 }
 
+emb_status emb_table_base(emb_ctx* ctx, int32_t k, int64_t* base) {
+  emb_status st = ctx_check(ctx);
+  if (st != EMB_OK) return st;
+  const int nt = ctx->cfg.num_tables > 0 ? ctx->cfg.num_tables : 1;
+  if (!base || k < 0 || k >= nt) return EMB_ERR_INVALID_ARG;
+  long long b = 0;
+  for (int i = 0; i < k; ++i) b += ctx->cfg.table_rows[i];
+  *base = b;
+  return EMB_OK;
+}
+
 emb_status emb_workspace_bytes(const emb_config* cfg, size_t* symmetric_bytes, size_t* local_bytes) {
   Plan pl;
   emb_status st = make_plan(cfg, &pl);
@@ -245,6 +266,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   // and how a prefetched N == 1 forward orders itself after its sort
   ctx->lc.fwd_per_sm = env_int("EMB_FWD_GRID_PER_SM", 4, 1, 32);
   ctx->sort_join = env_int("EMB_SORT_JOIN", 1, 0, 1) != 0;
+  ctx->fwd_dedup1 = env_int("EMB_FWD_DEDUP1", 0, 0, 1) != 0;  // measured slower at N == 1 (profiles/r02_tune/next3.txt)
 
   DevCtx& c = ctx->dc;
   memset(&c, 0, sizeof(c));
@@ -489,9 +511,12 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   const bool join = pre && ctx->pl.N == 1 && ctx->sort_join && ctx->sort_pending[p];
   if (join) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_sorted[p], 0));
   ctx->fwd_joined = join;
+  // N == 1 and joined: sort(t) is complete, so the forward may gather each
+  // distinct row once per reduce chunk (SURVEY §8(f) NEXT-3 forward dedup)
+  const int fdedup = (join && ctx->fwd_dedup1) ? 2 : dedup;
   CKC(ctx, gate(ctx, p, GATE_FWD, pre | (dedup << 1), stream));
   CKC(ctx, run_k(ctx, EMB_K_FWD, stream,
-                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, dedup, stream); }));
+                 [&] { return launch_fwd(ctx->dc, ctx->lc, ids, n, out, p, pre, fdedup, stream); }));
   if (!pre) {
     // ids were not prefetched: sort them now on the auxiliary stream (the
     // forward pushed them; the sort publishes the push to the peers)

@@ -91,8 +91,10 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
     src_base[v] = (c16 < c.cpr) ? shard_of(c, s) : nullptr;
     src_off[v] = (c16 - s * c.cps) * 16;
   }
-  if (dedup && c.fwd_dd[p]) {
-    // N > 1, prefetched, and the sort of this batch was complete at GATE_FWD: every distinct row is pulled once per reduce chunk (<= C equal
+  // dedup: 1 = N > 1, decided by GATE_FWD (fwd_dd[p]: sort(t) already complete);
+  //        2 = N == 1 with the stream joined on sort(t) (always complete)
+  if (dedup == 2 || (dedup == 1 && c.fwd_dd[p])) {
+    // prefetched, and the sort of this batch is complete: every distinct row is pulled once per reduce chunk (<= C equal
     // ids, ascending positions) and stored to all of the chunk's positions —
     // the NVLink bytes of the forward drop from T_r to ~(U_r + Zipf-head chunks)
     // rows (forward dedup).  Dropped keys (pad when

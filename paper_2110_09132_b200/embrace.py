@@ -31,7 +31,7 @@ EMB_STATE_SHARD, EMB_STATE_ADAM_M, EMB_STATE_ADAM_V = range(3)
 MODES = {"raw": EMB_BWD_RAW, "coal": EMB_BWD_COAL, "split": EMB_BWD_SPLIT}
 
 EXPORTED = [
-    "emb_status_str", "emb_workspace_bytes", "emb_create", "emb_ipc_handle", "emb_get_unique_id",
+    "emb_status_str", "emb_table_base", "emb_workspace_bytes", "emb_create", "emb_ipc_handle", "emb_get_unique_id",
     "emb_shard_init", "emb_sym_base", "emb_shard_init_colocated", "emb_forward_exchange", "emb_prefetch", "emb_backward_exchange", "dense_allreduce_enqueue",
     "dense_queue_flush", "dense_wait", "emb_flush", "emb_join", "emb_profile", "emb_profile_read",
     "emb_get_stats", "emb_debug_copy", "emb_state_ptr", "emb_queue_issue_order", "emb_shard_destroy",
@@ -51,7 +51,8 @@ class EmbConfig(ctypes.Structure):
                 ("max_tokens", ctypes.c_int32), ("mode", ctypes.c_int32), ("optim", ctypes.c_int32),
                 ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
                 ("eps", ctypes.c_float), ("grad_scale", ctypes.c_float), ("pad_id", ctypes.c_int64),
-                ("queue_window", ctypes.c_int32), ("timeout_ms", ctypes.c_int32)]
+                ("queue_window", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
+                ("num_tables", ctypes.c_int32), ("table_rows", ctypes.c_int64 * 8)]
 
 
 class EmbStats(ctypes.Structure):
@@ -85,6 +86,7 @@ def lib():
             "emb_workspace_bytes": [ctypes.POINTER(EmbConfig), ctypes.POINTER(ctypes.c_size_t),
                                     ctypes.POINTER(ctypes.c_size_t)],
             "emb_create": [ctypes.POINTER(EmbConfig), ctypes.POINTER(vp)],
+            "emb_table_base": [vp, i32, ctypes.POINTER(i64)],
             "emb_ipc_handle": [vp, u8p],
             "emb_get_unique_id": [u8p],
             "emb_shard_init": [vp, u8p, u8p, vp, vp],
@@ -139,10 +141,12 @@ def _bytes_arg(b):
 
 def make_config(vocab, dim, world=1, rank=0, device=0, dtype="fp32", max_tokens=4096, mode="split",
                 optim="sgd", lr=0.1, beta1=0.9, beta2=0.999, eps=1e-8, grad_scale=0.0, pad_id=-1,
-                queue_window=1, timeout_ms=10000):
+                queue_window=1, timeout_ms=10000, table_rows=None):
+    tr = list(table_rows or [])
     return EmbConfig(vocab, dim, world, rank, device, EMB_BF16 if dtype == "bf16" else EMB_FP32, max_tokens,
                      MODES[mode] if isinstance(mode, str) else mode, OPTIMS[optim],
-                     lr, beta1, beta2, eps, grad_scale, pad_id, queue_window, timeout_ms)
+                     lr, beta1, beta2, eps, grad_scale, pad_id, queue_window, timeout_ms,
+                     len(tr), (ctypes.c_int64 * 8)(*(tr + [0] * (8 - len(tr)))))
 
 
 # ---------------------------------------------------------------- C names
@@ -154,6 +158,12 @@ def emb_workspace_bytes(cfg):
     a, b = ctypes.c_size_t(), ctypes.c_size_t()
     _ck(lib().emb_workspace_bytes(ctypes.byref(cfg), ctypes.byref(a), ctypes.byref(b)), "emb_workspace_bytes")
     return a.value, b.value
+
+
+def emb_table_base(ctx, k):
+    b = ctypes.c_int64()
+    _ck(lib().emb_table_base(ctx, int(k), ctypes.byref(b)), "emb_table_base")
+    return b.value
 
 
 def emb_create(cfg):

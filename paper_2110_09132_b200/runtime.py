@@ -39,10 +39,11 @@ class EmbraceExchange:
 
     def __init__(self, vocab, dim, shard_init, *, world=1, rank=0, device=None, dtype="fp32",
                  max_tokens=4096, mode="split", optim="sgd", lr=0.1, beta1=0.9, beta2=0.999, eps=1e-8,
-                 grad_scale=0.0, pad_id=-1, queue_window=1, dense_queue=False, timeout_ms=10000, group=None):
+                 grad_scale=0.0, pad_id=-1, queue_window=1, dense_queue=False, timeout_ms=10000, group=None,
+                 table_rows=None):
         device = torch.cuda.current_device() if device is None else device
         self.cfg = E.make_config(vocab, dim, world, rank, device, dtype, max_tokens, mode, optim, lr, beta1, beta2,
-                                 eps, grad_scale, pad_id, queue_window, timeout_ms)
+                                 eps, grad_scale, pad_id, queue_window, timeout_ms, table_rows)
         self.world, self.rank, self.dim, self.vocab = world, rank, dim, vocab
         self.d = dim // world
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
@@ -104,6 +105,10 @@ class EmbraceExchange:
 
     def dense_wait(self, ticket, stream=None):
         E.dense_wait(self.ctx, ticket, stream)
+
+    def table_base(self, k):
+        """First global row of table k (stacked tables, embrace.h num_tables)."""
+        return E.emb_table_base(self.ctx, k)
 
     def sym_base(self):
         return E.emb_sym_base(self.ctx)

@@ -76,12 +76,13 @@ class Ranks:
     """The exchange contexts this process drives and their streams."""
 
     def __init__(self, cfg, N, ranks, shards, device, colocated, mode, optim, lr, pad_id, max_tokens,
-                 own_streams=False):
+                 own_streams=False, table_rows=None):
         import torch
         from paper_2110_09132_b200.runtime import EmbraceExchange, make_colocated
         self.N, self.ranks, self.colocated = N, list(ranks), colocated
         dev = torch.device("cuda", device)
-        kw = dict(dtype=cfg.dtype, max_tokens=max_tokens, mode=mode, optim=optim, lr=lr, pad_id=pad_id)
+        kw = dict(dtype=cfg.dtype, max_tokens=max_tokens, mode=mode, optim=optim, lr=lr, pad_id=pad_id,
+                  table_rows=table_rows)
         if colocated or own_streams:
             self.streams = make_streams(len(self.ranks), device)
         if colocated:
@@ -131,7 +132,7 @@ def _gather_state(rk, rows, optim):
 
 def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad_id=-1, last_none=True,
                device=0, rows_sample=None, ids_override=None, check=True, report=None, prefetch=False,
-               colocated=False, free=False, pipelined=False, null_at=()):
+               colocated=False, free=False, pipelined=False, null_at=(), table_rows=None):
     """Run `iters` iterations on the local rank(s) and assert parity (see the
     module docstring for the schedules).  null_at: iterations (0-based) whose
     backward gets next_ids = NULL although more iterations follow (D_next = ∅
@@ -158,7 +159,7 @@ def parity_run(cfg, N=1, rank=0, mode="split", iters=3, optim=None, lr=None, pad
     d = cfg.D // N
     max_tokens = max(cfg.max_tokens, max(len(x) for it in wl.ids for x in it))
     ranks = list(range(N)) if colocated else [rank]
-    rk = Ranks(cfg, N, ranks, shards, device, colocated, mode, optim, lr, pad_id, max_tokens)
+    rk = Ranks(cfg, N, ranks, shards, device, colocated, mode, optim, lr, pad_id, max_tokens, table_rows=table_rows)
     errs = {"W": 0.0, "m": 0.0, "v": 0.0, "dW_ulp": 0.0}
     fwd_bytes = {r: np.zeros(N, np.int64) for r in ranks}
     bwd_bytes = {r: np.zeros(N, np.int64) for r in ranks}

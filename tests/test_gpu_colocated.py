@@ -95,3 +95,12 @@ def test_graph_replay_colocated():
 def test_adagrad_colocated(n):
     parity_run(get_config("tiny"), N=n, mode="split", iters=3, optim="adagrad", lr=0.05, colocated=True)
     parity_run(_small("bert_large", 2), N=n, mode="split", iters=3, optim="adagrad", lr=1e-2, colocated=True)
+
+
+def test_two_tables_colocated():
+    """GNMT-like: encoder and decoder tables of one width in one exchange (NEXT-3)."""
+    from synthetic.workloads import Config
+    from test_gpu_parity import _two_tables
+    cfg = Config("twotab", 1000, 64, "bf16", 8, 16, 8, optim="adam", lr=1e-2)
+    parity_run(cfg, N=2, mode="split", iters=3, ids_override=_two_tables(600), table_rows=(600, 400),
+               prefetch=True, colocated=True)

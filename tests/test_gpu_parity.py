@@ -210,3 +210,30 @@ def test_adagrad_tiny(mode):
 
 def test_adagrad_bf16_paper_shape_free_running():
     parity_run(_small("gnmt", batch=8), N=1, mode="split", iters=6, optim="adagrad", lr=1e-2, free=True)
+
+
+# ---------------------------------------------------------------- NEXT-3: several tables, one exchange
+
+def _two_tables(L1):
+    """ids override: each rank's first half looks up table A (rows [0, L1)), the
+    second half table B (rows [L1, L)): global row ids, as embrace.h prescribes."""
+    def f(ids):
+        out = []
+        for it in ids:
+            row = []
+            for x in it:
+                x = np.asarray(x, np.int64).copy()
+                h = x.size // 2
+                x[:h] = x[:h] % L1
+                x[h:] = L1 + (x[h:] % (1000 - L1))
+                row.append(x.astype(np.int32))
+            out.append(row)
+        return out
+    return f
+
+
+@pytest.mark.parametrize("prefetch", [False, True])
+def test_two_tables_one_exchange(prefetch):
+    cfg = Config("twotab", 1000, 16, "fp32", 8, 16, 8, optim="adam", lr=1e-2)
+    parity_run(cfg, N=1, mode="split", iters=4, ids_override=_two_tables(600), table_rows=(600, 400),
+               prefetch=prefetch)

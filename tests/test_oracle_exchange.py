@@ -209,3 +209,41 @@ def test_oracle_lm_sized_sample_runs():
     m, v = [np.zeros_like(W)], [np.zeros_like(W)]
     res = exchange.simulate_iteration([W], wl.ids[0], wl.dY[0], wl.ids[1], 1, "split", "fp32", ADAM, m, v)
     assert res.u[0] < res.T[0] and 0 < res.p[0] < res.u[0]
+
+
+# ---------------------------------------------------------------- NEXT-3: several tables in one exchange
+
+@pytest.mark.parametrize("mode", ["raw", "split"])
+def test_stacked_tables_equal_separate_exchanges(mode):
+    """Reading for SURVEY §8(f) NEXT-3 (PAPER.md:481 two LM tables; PAPER.md:319-320
+    GNMT encoder / decoder tables): tables of one width stacked row-wise form ONE
+    exchange over global row ids (local id + table base).  Pinned here: that
+    exchange gives every table exactly what its own exchange gives (the row sets
+    are disjoint, so sums, splits and updates are per table)."""
+    rng = np.random.default_rng(31)
+    L1, L2, D, N = 50, 30, 8, 2
+    A = rng.uniform(-1, 1, (L1, D))
+    B = rng.uniform(-1, 1, (L2, D))
+    ia = [rng.integers(0, L1, 12) for _ in range(N)]
+    ib = [rng.integers(0, L2, 7) for _ in range(N)]
+    ga = [rng.uniform(-1, 1, (12, D)) for _ in range(N)]
+    gb = [rng.uniform(-1, 1, (7, D)) for _ in range(N)]
+    na = [rng.integers(0, L1, 5) for _ in range(N)]
+    nb_ = [rng.integers(0, L2, 5) for _ in range(N)]
+    # stacked: one exchange, global ids (B's rows after A's)
+    S = partition.partition_columnwise(np.vstack([A, B]), N)
+    ids = [np.concatenate([ia[r], L1 + ib[r]]) for r in range(N)]
+    dY = [np.vstack([ga[r], gb[r]]) for r in range(N)]
+    nxt = [np.concatenate([na[r], L1 + nb_[r]]) for r in range(N)]
+    res = exchange.simulate_iteration(S, ids, dY, nxt, 1, mode, "fp64", SGD)
+    # separate exchanges
+    SA = partition.partition_columnwise(A.copy(), N)
+    SB = partition.partition_columnwise(B.copy(), N)
+    ra = exchange.simulate_iteration(SA, ia, ga, na, 1, mode, "fp64", SGD)
+    rb = exchange.simulate_iteration(SB, ib, gb, nb_, 1, mode, "fp64", SGD)
+    for r in range(N):
+        np.testing.assert_array_equal(res.Y[r][:12], ra.Y[r])
+        np.testing.assert_array_equal(res.Y[r][12:], rb.Y[r])
+    np.testing.assert_array_equal(np.hstack(S)[:L1], np.hstack(SA))
+    np.testing.assert_array_equal(np.hstack(S)[L1:], np.hstack(SB))
+    assert res.U.tolist() == ra.U.tolist() + (L1 + rb.U).tolist()
