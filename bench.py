@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="lstm_lm")
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
+    ap.add_argument("--schedule", action="store_true",
+                    help="NEXT-1: Computation Stall of FIFO / Horizontal / 2D scheduling (separate JSON line)")
     ap.add_argument("--tables", type=int, default=1, choices=[1, 2],
                     help="NEXT-3: exchange this many stacked tables (same shape) in one call")
     ap.add_argument("--optim", default=None, choices=["sgd", "adam", "adagrad"],
@@ -492,6 +494,152 @@ def run_dense(args, cfg, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------- NEXT-1: 2D schedule and Computation Stall
+def run_schedule(args, cfg, world, rank, local):
+    """SURVEY §8(f) NEXT-1 (PAPER.md:282-336 Horizontal / Vertical / 2D
+    Scheduling, PAPER.md:542-550 Computation Stall).  A synthetic training step
+    around the real exchange: embedding FP (emb_forward_exchange), K dense
+    blocks' FP (GEMM stand-ins, block k = one [T, H] x [H, H] bf16 GEMM of the
+    config's dense-block size), their BP in reverse (two GEMMs each; the weight
+    gradient's AllReduce enqueued into the a13 priority queue as soon as it is
+    produced, priority = FP order), embedding BP (emb_backward_exchange).  The
+    FP of block k of the next iteration consumes block k's averaged gradient.
+      fifo        Default Scheduling: queue window 1 (issue in BP order), COAL
+                  exchange, and the next FP waits for EVERY AllReduce
+                  (PAPER.md:323-325);
+      horizontal  priority queue (window = K: issued at the end of BP in FP
+                  order), the next iteration's embedding FP first, block k's FP
+                  waits only for block k's AllReduce; COAL (PAPER.md:327-336);
+      2d          horizontal + Vertical Scheduling (SPLIT: only the prior part
+                  precedes the next FP, the deferred part on the lowest-priority
+                  side stream).
+    Computation Stall = step time - compute-only step time (the same GEMMs, no
+    exchange, no AllReduce): the GPU idle time plus, for 2d, the Vertical
+    Scheduling computation.  Device time on the main stream,
+    CUDA events, max over ranks."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2110_09132_b200 import embrace as E
+    from paper_2110_09132_b200.runtime import EmbraceExchange
+
+    K = cfg.dense_blocks or 16
+    H = 2048
+    H2 = max(256, (cfg.dense_block_elems or 8_400_000) // H // 128 * 128)  # block weight [H, H2] ~ the config's size
+    nb = 4
+    ids, ids_all, dY = make_batches(cfg, world, rank, nb)
+    T = min(len(x) for x in ids)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    ids_d = [torch.from_numpy(x).to(dev) for x in ids]
+    dY_d = [torch.from_numpy(x).to(dev).to(tdt) for x in dY]
+    Y_d = [torch.empty((len(x), cfg.D), dtype=tdt, device=dev) for x in ids]
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    Wb = [torch.randn(H, H2, device=dev, dtype=torch.bfloat16, generator=g) * 0.01 for _ in range(K)]
+    Wb2 = [torch.randn(H2, H, device=dev, dtype=torch.bfloat16, generator=g) * 0.01 for _ in range(K)]
+    Gb = [torch.zeros(H, H2, device=dev, dtype=torch.bfloat16) for _ in range(K)]
+    stream = torch.cuda.current_stream()
+    d = cfg.D // world
+    Wt = gen_table_t(cfg)
+    shard0 = torch.from_numpy(np.ascontiguousarray(Wt[:, rank * d:(rank + 1) * d])).to(dev).to(tdt)
+    del Wt
+
+    def x_from(Y):  # the blocks' input: the embedding rows (width D) tiled / cut to H
+        x = Y[:T].to(torch.bfloat16)
+        return x.repeat(1, (H + cfg.D - 1) // cfg.D)[:, :H].contiguous()
+
+    def step_compute(k, ex, sched, tickets):
+        b = k % nb
+        nxt = ids_d[(b + 1) % nb]
+        if ex is not None:
+            if sched == "fifo":
+                for tk in tickets:                       # Default: every AllReduce before the next FP
+                    E.dense_wait(ex.ctx, tk, stream)
+            E.emb_prefetch(ex.ctx, nxt, stream)
+            E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], stream)   # embedding FP first (PAPER.md:335)
+            x = x_from(Y_d[b])
+        else:
+            x = x_from(Y_d[b])
+        acts = []
+        for j in range(K):                                # dense FP, block j needs its averaged gradient
+            if ex is not None and sched != "fifo" and tickets:
+                E.dense_wait(ex.ctx, tickets[j], stream)
+            acts.append(x)
+            x = torch.relu(x @ Wb[j]) @ Wb2[j]
+        dx = x
+        ready = []
+        new_tickets = [None] * K
+        for j in reversed(range(K)):                      # dense BP: weight grad, then its AllReduce
+            h = torch.relu(acts[j] @ Wb[j])
+            dh = dx @ Wb2[j].t()
+            torch.matmul(acts[j].t(), dh, out=Gb[j])
+            dx = dh @ Wb[j].t()
+            if ex is not None:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                ready.append(ev)                          # borrowed by the queue until issued
+                new_tickets[j] = E.dense_allreduce_enqueue(ex.ctx, Gb[j], j, ev)
+            del h
+        if ex is not None:
+            E.emb_backward_exchange(ex.ctx, dY_d[b], nxt, stream)   # embedding BP (sparse exchange)
+            E.dense_queue_flush(ex.ctx)
+        return new_tickets, ready
+
+    def timed(ex, sched, iters, warm):
+        tickets, keep = [], []
+        for k in range(warm):
+            tickets, r = step_compute(k, ex, sched, tickets)
+            keep.append(r)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(warm, warm + iters):
+            tickets, r = step_compute(k, ex, sched, tickets)
+            keep.append(r)
+        if ex is not None:
+            for tk in tickets:
+                E.dense_wait(ex.ctx, tk, stream)
+            E.emb_join(ex.ctx, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms * 1e3
+
+    iters, warm = max(5, min(args.steps, 30)), max(3, min(args.warmup, 5))
+    compute_us = timed(None, None, iters, warm)
+    res = {}
+    for sched, mode, window in (("fifo", "coal", 1), ("horizontal", "coal", K), ("2d", "split", K)):
+        ex = EmbraceExchange(cfg.L, cfg.D, shard0, world=world, rank=rank, device=local, dtype=cfg.dtype,
+                             max_tokens=cfg.max_tokens, mode=mode, optim=cfg.optim, lr=cfg.lr, dense_queue=True,
+                             queue_window=window)
+        step_us = timed(ex, sched, iters, warm)
+        ex.flush()
+        ex.close()
+        res[sched] = {"step_us": round(step_us, 1), "stall_us": round(step_us - compute_us, 1),
+                      "sparse_mode": mode, "queue_window": window}
+    if rank == 0:
+        line = {"metric": "2D-schedule computation stall (NEXT-1): step time - compute-only time",
+                "value": res["2d"]["stall_us"], "unit": "us per iteration", "n_gpus": world, "steps": iters,
+                "warmup": warm, "higher_is_better": False, "dtype": cfg.dtype, "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: embedding exchange + {K} dense blocks "
+                                       f"([{T}, {H}] x [{H}, {H2}] bf16 GEMM pairs), per-block AllReduce "
+                                       f"{H * H2 * 2 / 2**20:.1f} MiB bf16"},
+                "compute_only_us": round(compute_us, 1), "schedules": res,
+                "stall_ratio_fifo_over_2d": round(res["fifo"]["stall_us"] / res["2d"]["stall_us"], 3)
+                if res["2d"]["stall_us"] > 0 else None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -507,6 +655,8 @@ def main():
         return run_reference(args, cfg, world, rank)
     if args.dense_queue:
         return run_dense(args, cfg, world, rank, local)
+    if args.schedule:
+        return run_schedule(args, cfg, world, rank, local)
 
     import torch
     torch.cuda.set_device(local)

@@ -237,3 +237,11 @@ def test_two_tables_one_exchange(prefetch):
     cfg = Config("twotab", 1000, 16, "fp32", 8, 16, 8, optim="adam", lr=1e-2)
     parity_run(cfg, N=1, mode="split", iters=4, ids_override=_two_tables(600), table_rows=(600, 400),
                prefetch=prefetch)
+
+
+def test_forward_dedup_n1_knob(monkeypatch):
+    """EMB_FWD_DEDUP1=1: the N == 1 forward gathers each distinct row once per
+    reduce chunk (measured slower, default off): Y still exact."""
+    monkeypatch.setenv("EMB_FWD_DEDUP1", "1")
+    parity_run(get_config("tiny"), N=1, mode="split", iters=4, prefetch=True)
+    parity_run(_small("lstm_lm", batch=8), N=1, mode="split", iters=3, prefetch=True, rows_sample=512)
