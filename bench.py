@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="lstm_lm")
     ap.add_argument("--mode", default="split", choices=["raw", "coal", "split"])
+    ap.add_argument("--baseline", default=None, choices=["allgather", "allreduce"],
+                    help="NEXT-2: time an in-box baseline (baselines/inbox.py) instead of the exchange")
     ap.add_argument("--schedule", action="store_true",
                     help="NEXT-1: Computation Stall of FIFO / Horizontal / 2D scheduling (separate JSON line)")
     ap.add_argument("--tables", type=int, default=1, choices=[1, 2],
@@ -640,6 +642,73 @@ def run_schedule(args, cfg, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------- NEXT-2: in-box baselines
+def run_baseline(args, cfg, world, rank, local):
+    """the same workload through baselines/inbox.py
+    (Horovod-AllGather-style sparse aggregation or dense-gradient AllReduce, a
+    replicated table per rank, torch ops + NCCL), timed like the main arm
+    (CUDA events, max over ranks; eager: the collectives' sizes are host-side).
+    One JSON line, impl "inbox_<kind>"; compare with the main arm's value."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from baselines.inbox import ReplicatedTable
+    nb = n_batches(cfg, world)
+    ids, ids_all, dY = make_batches(cfg, world, rank, nb)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    ids_d = [torch.from_numpy(x.astype(np.int64)).to(dev) for x in ids]
+    dY_d = [torch.from_numpy(x).to(dev).to(tdt) for x in dY]
+    W = torch.from_numpy(gen_table_t(cfg)).to(dev).to(tdt)
+    rt = ReplicatedTable(W, optim=cfg.optim, lr=cfg.lr, world=world, kind=args.baseline)
+    del W
+    stream = torch.cuda.current_stream()
+
+    def step(k):
+        b = k % nb
+        rt.forward(ids_d[b])
+        rt.backward(ids_d[b], dY_d[b], cfg.max_tokens)
+
+    for k in range(args.warmup):
+        step(k)
+    K = min(args.steps, 200)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for j in range(K):
+            step(args.warmup + j)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    tok = sum(count_nonpad(ids_all[(args.warmup + j) % nb][s]) for j in range(K) for s in range(world))
+    esz = 2 if cfg.dtype == "bf16" else 4
+    wire = ((world - 1) * cfg.max_tokens * (cfg.D * esz + 8) if args.baseline == "allgather"
+            else 2 * (world - 1) / world * cfg.L * cfg.D * 4) if world > 1 else 0
+    if rank == 0:
+        line = {"metric": METRIC, "value": tok / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "bf16"}[cfg.dtype], "data": "synthetic",
+                "impl": f"inbox_{args.baseline}",
+                "config": {"workload": f"{cfg.name}: L={cfg.L} D={cfg.D} {cfg.dtype}, replicated table per rank",
+                           "aggregation": {"allgather": "all_gather_into_tensor of every rank's padded (ids, dY) "
+                                                        "+ local coalesce (Horovod AllGather)",
+                                           "allreduce": "dense [L, D] fp32 gradient AllReduce (Horovod dense)"}
+                           [args.baseline], "optim": cfg.optim},
+                "wire_bytes_per_rank_per_step": int(wire), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -657,6 +726,8 @@ def main():
         return run_dense(args, cfg, world, rank, local)
     if args.schedule:
         return run_schedule(args, cfg, world, rank, local)
+    if args.baseline:
+        return run_baseline(args, cfg, world, rank, local)
 
     import torch
     torch.cuda.set_device(local)
