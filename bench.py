@@ -134,6 +134,29 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ---------------------------------------------------------------- NVLink traffic (NVML counters)
+def nvlink_kib(local):
+    """Cumulative NVLink data KiB (TX, RX) of this rank's GPU over all links
+    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX), or None."""
+    try:
+        import pynvml as nv
+        import torch
+        nv.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(local)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            h = nv.nvmlDeviceGetHandleByIndex(local)
+        vals = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                               nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        if any(v.nvmlReturn != 0 for v in vals):
+            return None
+        return [int(v.value.ullVal) for v in vals]
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- workload
 def n_batches(cfg, N):
     """Enough distinct batches that the inputs+outputs cycled through exceed
@@ -812,6 +835,8 @@ def main():
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st0 = ex.stats() if world > 1 else None
+    nv0 = nvlink_kib(local) if world > 1 else None
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(n_rep):
@@ -821,8 +846,25 @@ def main():
         E.emb_join(ex.ctx, stream)
         ev1.record(stream)
         torch.cuda.synchronize()
+    nv1 = nvlink_kib(local) if world > 1 else None
     barrier()
     ms = ev0.elapsed_time(ev1)
+    nvl_meas = None
+    if world > 1:
+        st1 = ex.stats()
+        remote = {k: sum(st1[k][s_] - st0[k][s_] for s_ in range(world) if s_ != rank) / K
+                  for k in ("fwd_bytes_pulled", "bwd_bytes_pushed", "ids_bytes_pushed")}
+        nvl_meas = {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (all links, KiB counters) around the timed region",
+                    "library_counters_per_step": {k: int(v) for k, v in remote.items()},
+                    "library_note": "emb_get_stats deltas to/from peers: forward bytes PULLED (arrive as RX), "
+                                    "gradient + id bytes PUSHED (leave as TX)"}
+        if nv0 and nv1:
+            tx, rx = (nv1[0] - nv0[0]) * 1024 / K, (nv1[1] - nv0[1]) * 1024 / K
+            nvl_meas.update({"tx_bytes_per_step": int(tx), "rx_bytes_per_step": int(rx),
+                             "tx_gbs": round(tx / (ms / K * 1e-3) / 1e9, 1),
+                             "rx_gbs": round(rx / (ms / K * 1e-3) / 1e9, 1)})
+        else:
+            nvl_meas["unavailable"] = "NVML NVLink throughput fields not readable on this host"
     check_err("timed region")
     if os.environ.get("EMB_TRACE_OUT"):  # kernel trace ring (EMB_TRACE builds; scripts/trace.py)
         np.save(f"{os.environ['EMB_TRACE_OUT']}.{rank}.npy", E.emb_debug_copy(ex.ctx, E.EMB_DBG_TIMESTAMPS))
@@ -1082,6 +1124,7 @@ def main():
                                                  "frac": round(t_roof_plain_us / (ms_per_step * 1e3), 4),
                                                  "fwd_nvlink_convention": "SURVEY §8(d): (N-1) T_r d e"}},
             "step_time": dist_t,
+            "nvlink_measured": nvl_meas,
             "kernels": kern,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
