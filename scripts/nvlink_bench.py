@@ -9,8 +9,6 @@ Per message size (bytes per peer pair, the exchange's range):
   * NCCL all_to_all_single (the library AlltoAll the paper uses):
     algorithm bandwidth per rank = bytes sent to peers / time, and the
     per-direction NVLink rate of one GPU;
-  * copy-engine peer copy (cudaMemcpyPeerAsync via torch, rank 0 -> rank 1):
-    the measured point-to-point rate.
 Device time with CUDA events, max over ranks.  One JSON line on rank 0.
 """
 
@@ -27,7 +25,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    out = {"n_gpus": world, "alltoall": [], "peer_copy": []}
+    out = {"n_gpus": world, "alltoall": []}
     for per_pair in (256 << 10, 1 << 20, 4 << 20, 16 << 20):
         n = per_pair * world // 4
         x = torch.ones(n, dtype=torch.float32, device=dev)
@@ -49,26 +47,6 @@ def main():
         sent = per_pair * (world - 1)
         out["alltoall"].append({"bytes_per_pair": per_pair, "us": round(ms * 1e3, 2),
                                 "gbs_per_rank_out": round(sent / (ms * 1e-3) / 1e9, 1)})
-    if rank == 0 and world > 1 and torch.cuda.device_count() > 1:
-        src = dev
-        dst = torch.device("cuda", (local + 1) % torch.cuda.device_count())
-        for size in (1 << 20, 16 << 20, 256 << 20):
-            a = torch.ones(size // 4, dtype=torch.float32, device=src)
-            b = torch.empty(size // 4, dtype=torch.float32, device=dst)
-            for _ in range(3):
-                b.copy_(a, non_blocking=True)
-            torch.cuda.synchronize(src)
-            torch.cuda.synchronize(dst)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            it = 20
-            e0.record()
-            for _ in range(it):
-                b.copy_(a, non_blocking=True)
-            e1.record()
-            torch.cuda.synchronize(src)
-            ms = e0.elapsed_time(e1) / it
-            out["peer_copy"].append({"bytes": size, "us": round(ms * 1e3, 1),
-                                     "gbs": round(size / (ms * 1e-3) / 1e9, 1)})
     if rank == 0:
         out["note"] = ("alltoall gbs_per_rank_out = bytes each rank sends to its N-1 peers / time (the exchange's "
                        "per-GPU NVLink injection); nominal 900 GB/s per direction, guide-measured peer copy 770")
