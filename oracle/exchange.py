@@ -98,6 +98,19 @@ def _grad_terms(ids, dY, pad_id):
     return ids, dY
 
 
+def _quot_sigma(a, num, mu_num, den2, mu_den2, eps):
+    """First-order error magnitude of q = a * num / (sqrt(den2) + eps) when num
+    and den2 carry errors proportional to the magnitudes mu_num, mu_den2 of the
+    terms summed into them (reading B12):
+        |dq| <= a mu_num / (sqrt(den2) + eps) + a num mu_den2 / (2 sqrt(den2) (sqrt(den2) + eps)^2).
+    The second term is 0 where den2 == 0 (then num == 0 too)."""
+    sd = np.sqrt(den2)
+    t1 = a * mu_num / (sd + eps)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t2 = np.where(sd > 0, a * num * mu_den2 / (2 * sd * (sd + eps) ** 2), 0.0)
+    return t1 + t2
+
+
 def simulate_iteration(shards, ids, dY, next_ids, t, mode="split", dtype="fp32",
                        opt=None, m=None, v=None, pad_id=-1):
     """One iteration on N simulated workers.
@@ -216,6 +229,8 @@ def simulate_iteration(shards, ids, dY, next_ids, t, mode="split", dtype="fp32",
             g_r = scale * acc
             sg_r = abs(scale) * sab
             old_W = np.asarray(shards[r][rows], np.float64)
+            m_old = np.asarray(m[r][rows], np.float64) if opt.kind in ("adam", "adagrad") else None
+            v_old = np.asarray(v[r][rows], np.float64) if opt.kind == "adam" else None
             if opt.kind == "sgd":
                 optim.sgd_apply(shards[r], rows, g_r, opt.lr, store=dtype)
             elif opt.kind == "adagrad":
@@ -230,15 +245,33 @@ def simulate_iteration(shards, ids, dY, next_ids, t, mode="split", dtype="fp32",
             if opt.kind == "sgd":
                 res.sigma_W[at, c0:c1] = np.abs(old_W) + opt.lr * sg_r
             elif opt.kind == "adagrad":
-                res.sigma_W[at, c0:c1] = np.abs(old_W) + np.abs(new_W - old_W)
+                s_new = np.asarray(m[r][rows], np.float64)
+                # dW = lr g / (sqrt(s) + eps): first-order error magnitude from g (sigma_g) and from
+                # s = s_old + g^2 (reading B12)
+                # (|dW| <= lr for any g: the bound is capped at 2 lr where it is ill-conditioned)
+                res.sigma_W[at, c0:c1] = (np.abs(old_W) + np.abs(new_W - old_W)
+                                          + np.minimum(2 * opt.lr, _quot_sigma(
+                                              opt.lr, np.abs(g_r), sg_r, s_new,
+                                              np.abs(m_old) + g_r * g_r + 2 * np.abs(g_r) * sg_r, opt.eps)))
                 # accumulator s += g^2: first-order magnitude |s| + 2 |g| sigma_g
-                res.sigma_m[at, c0:c1] = (np.abs(np.asarray(m[r][rows], np.float64))
-                                          + 2 * np.abs(g_r) * sg_r)
+                res.sigma_m[at, c0:c1] = s_new + 2 * np.abs(g_r) * sg_r
             else:
-                res.sigma_W[at, c0:c1] = np.abs(old_W) + np.abs(new_W - old_W)
-                res.sigma_m[at, c0:c1] = np.abs(np.asarray(m[r][rows], np.float64)) + (1 - opt.beta1) * sg_r
-                res.sigma_v[at, c0:c1] = (np.abs(np.asarray(v[r][rows], np.float64))
-                                          + 2 * (1 - opt.beta2) * np.abs(g_r) * sg_r)
+                m_new = np.asarray(m[r][rows], np.float64)
+                v_new = np.asarray(v[r][rows], np.float64)
+                a_t = optim.adam_alpha(t, opt.lr, opt.beta1, opt.beta2)
+                # dW = alpha m / (sqrt(v) + eps): first-order error magnitude from the magnitudes
+                # summed into m and v (not only |dW|: m cancels when g opposes m; reading B12)
+                mu_m = (2 - opt.beta1) * np.abs(m_old) + (1 - opt.beta1) * sg_r
+                mu_v = (2 - opt.beta2) * np.abs(v_old) + (1 - opt.beta2) * (g_r * g_r + 2 * np.abs(g_r) * sg_r)
+                # (|m| / sqrt(v) <= (1-b1) / sqrt((1-b2)(1-b1^2/b2)) for any gradient history, so |dW| is
+                # bounded; the first-order term is capped at twice that bound where it is ill-conditioned,
+                # e.g. an exactly cancelled g with v = 0)
+                step_max = a_t * (1 - opt.beta1) / np.sqrt((1 - opt.beta2) * (1 - opt.beta1 ** 2 / opt.beta2))
+                res.sigma_W[at, c0:c1] = (np.abs(old_W) + np.abs(new_W - old_W)
+                                          + np.minimum(2 * step_max,
+                                                       _quot_sigma(a_t, np.abs(m_new), mu_m, v_new, mu_v, opt.eps)))
+                res.sigma_m[at, c0:c1] = np.abs(m_new) + (1 - opt.beta1) * sg_r
+                res.sigma_v[at, c0:c1] = v_new + 2 * (1 - opt.beta2) * np.abs(g_r) * sg_r
 
     # S8 — byte counters: forward (r -> s) = T_s d_r e; backward (n -> r) =
     # c_n d_r e with c_n = T_n (raw), u_n (coal), p_n + q_n (split); ids T_r * 4

@@ -18,6 +18,13 @@ enum ErrBit { ERR_ID = 1, ERR_STATE = 2, ERR_TIMEOUT = 4 };
 // counts[p][n][CNT_W]
 //   written by sort(t):   T, U (unique kept ids), NCH (reduce chunks), NLONG (multi-chunk uniques)
 //   written by tables(t): P (prior uniques of the Alg. 1 split; stats / debug only)
+// chunk_desc[].w = chunks of the unique | (first position + 1) << DESC_POS_SHIFT for
+// a single-row unique (its one position rides with the descriptor: the reduce
+// needs no perm load for it), 0 above the chunk count otherwise
+constexpr int DESC_POS_SHIFT = 13;
+constexpr int DESC_NCH_MASK = (1 << DESC_POS_SHIFT) - 1;
+__host__ __device__ __forceinline__ int desc_nch(int w) { return w & DESC_NCH_MASK; }
+__host__ __device__ __forceinline__ int desc_pos1(int w) { return (w >> DESC_POS_SHIFT) - 1; }
 enum CountSlot { CNT_T = 0, CNT_U = 1, CNT_P = 2, CNT_NCH = 3, CNT_NLONG = 4, CNT_W = 8 };
 
 // Peer-written flags living in every rank's NVLink-visible region.  Slot [n]

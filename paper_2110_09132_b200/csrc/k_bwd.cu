@@ -47,7 +47,7 @@ static constexpr int BWD_WARPS = BWD_THREADS / 32;
 // acc[v*EPV + i] = sum over rows perm[b..e) (ascending) of row[c16 = lane + 32 v]
 template <int DT, int V, bool PEER>
 __device__ __forceinline__ void reduce_rows(const char* __restrict__ base, size_t stride, int ncol16,
-                                            const int* __restrict__ perm, int b, int e, float* acc) {
+                                            const int* __restrict__ perm, int b, int e, float* acc, int pos1 = -1) {
   constexpr int EPV = Vec<DT>::EPV;
   constexpr int RB = EMB_RB;
   const int lane = threadIdx.x & 31;
@@ -58,7 +58,7 @@ __device__ __forceinline__ void reduce_rows(const char* __restrict__ base, size_
   for (int i = b; i < e; i += RB) {
     if (((i - b) & 31) == 0) {
       const int j = i + lane;
-      mypos = (j < e) ? __ldg(perm + j) : 0;
+      mypos = (pos1 >= 0) ? pos1 : ((j < e) ? __ldg(perm + j) : 0);  // pos1: a single-row chunk's position
     }
     int pos[RB];
 #pragma unroll
@@ -227,8 +227,9 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
   for (int ch = gw; ch < NCH; ch += nw) {
     const int4 dsc = desc[ch];  // {unique i, perm begin, perm end, chunks of i}
     float acc[V * EPV];
-    reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, dsc.y, dsc.z, acc);
-    store_partial<EPV, V>((dsc.w > 1) ? part + (size_t)ch * c.D : c.gcoal + (size_t)dsc.x * c.D, c.cpr, acc);
+    reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, dsc.y, dsc.z, acc, desc_pos1(dsc.w));
+    store_partial<EPV, V>((desc_nch(dsc.w) > 1) ? part + (size_t)ch * c.D : c.gcoal + (size_t)dsc.x * c.D, c.cpr,
+                          acc);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // gate duties folded into this kernel's CTA 0 (no gate kernel before the
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
       if (n == m && ch >= nchs[m]) { ch -= nchs[m]; n = m + 1; }
     const size_t bpn = pn(c, p, n) * (size_t)c.max_tok;
     const int4 dsc = c.chunk_desc[pn(c, p, n) * (size_t)c.max_chunks + ch];  // {k, begin, end, nch}
-    const int k = dsc.x, nch = dsc.w;
+    const int k = dsc.x, nch = desc_nch(dsc.w);
     reduce_rows<DT, V, true>(recv_of(c, c.r, p, n), slice_bytes, c.cps, c.perm + bpn, dsc.y, dsc.z, acc);
     float* dst = (nch > 1) ? c.scratch + (size_t)p * c.max_chunks * c.D + ((size_t)n * c.max_chunks + ch) * c.d
                            : c.gc_owner + (bpn + k) * (size_t)c.d;

@@ -343,8 +343,12 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
           lq_off[qs] = off;
         }
       }
-      if (qs < 0 || qs >= QMAX)
-        for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
+      if (qs < 0 || qs >= QMAX) {
+        if (b - a == 1)  // single-row unique: its position (the head key, in this CTA's slice) rides along
+          chunk_desc[off] = make_int4(k, a, b, 1 | ((int)(keyA[a - lo] & posmask) + 1) << DESC_POS_SHIFT);
+        else
+          for (int q = 0; q < nch; ++q) chunk_desc[off + q] = make_int4(k, a + q * c.C, min(b, a + (q + 1) * c.C), nch);
+      }
       if (nch > 1) long_u[lb + olong] = k;
     }
     cb += tch;

@@ -84,7 +84,20 @@ def test_sigma_hand_computed_cancellation():
             assert res.sigma_v[0, 0] == 0.0
             dW = shards[0][res.U] - W[res.U]
             assert dW[0, 0] == 0.0
-            np.testing.assert_allclose(res.sigma_W, np.abs(W[res.U]) + np.abs(dW), rtol=1e-15)
+            # sigma_W (reading B12): |W| + |dW| + the first-order error of alpha m / (sqrt(v) + eps)
+            # from the magnitudes summed into m and v, capped at twice Adam's largest possible step;
+            # at the cancelled element (v = 0, denominator eps) it is the cap
+            a1 = 1e-3 * np.sqrt(1 - B2) / (1 - B1)
+            cap = 2 * a1 * (1 - B1) / np.sqrt((1 - B2) * (1 - B1 ** 2 / B2))
+            sg = res.sigma_g
+            mu_m = (1 - B1) * sg
+            mu_v = (1 - B2) * (g * g + 2 * np.abs(g) * sg)
+            sv = np.sqrt(v1)
+            first = a1 * mu_m / (sv + 1e-8) + np.where(sv > 0, a1 * m1 * mu_v / (2 * np.where(sv > 0, sv, 1)
+                                                                                   * (sv + 1e-8) ** 2), 0)
+            want = np.abs(W[res.U]) + np.abs(dW) + np.minimum(cap, first)
+            np.testing.assert_allclose(res.sigma_W, want, rtol=1e-12)
+            assert res.sigma_W[0, 0] == pytest.approx(abs(W[5, 0]) + cap, rel=1e-12)
 
 
 def test_sigma_bounds_fp32_summation_error():
@@ -129,7 +142,48 @@ def test_sigma_adam_closed_form_step1():
     g = res.g
     dW = -1e-3 * g / (np.abs(g) + 1e-8 / np.sqrt(1 - B2))
     np.testing.assert_allclose(shards[0][res.U] - W[res.U], dW, rtol=1e-9, atol=1e-18)
-    np.testing.assert_allclose(res.sigma_W, np.abs(W[res.U]) + np.abs(dW), rtol=1e-9)
+    # sigma_W >= |W_old| + |dW|, and never more than that plus twice Adam's largest step
+    a1 = 1e-3 * np.sqrt(1 - B2) / (1 - B1)
+    cap = 2 * a1 * (1 - B1) / np.sqrt((1 - B2) * (1 - B1 ** 2 / B2))
+    base = np.abs(W[res.U]) + np.abs(dW)
+    assert np.all(res.sigma_W >= base * (1 - 1e-12)) and np.all(res.sigma_W <= base + cap * (1 + 1e-12))
+
+
+def _adam_fp32_like_gpu(w, m, v, g, alpha, b1=B1, b2=B2, eps=1e-8):
+    """One Adam element step in fp32 with the GPU kernel's operation order
+    (csrc/k_bwd.cu opt_math): m += (1-b1)(g-m); v += (1-b2)(g^2-v);
+    w -= alpha * m * (1 / (sqrt(v) + eps)), every operation rounded to fp32."""
+    f = np.float32
+    w, m, v, g, alpha = f(w), f(m), f(v), f(g), f(alpha)
+    m = f(m + f(f(1 - b1) * f(g - m)))
+    v = f(v + f(f(1 - b2) * f(f(g * g) - v)))
+    q = f(1) / f(f(np.sqrt(v)) + f(eps))
+    return float(f(w - f(f(alpha * m) * q))), float(m), float(v)
+
+
+def test_sigma_w_adam_covers_fp32_cancellation_in_m():
+    """The Adam sigma_W term of reading B12 is NEEDED and SUFFICIENT: when g
+    nearly cancels the previous m (m_new << |m_old|, |g|), an fp32 evaluation
+    in the GPU's operation order misses the fp64 result by far more than
+    1e-5 (|W_old| + |dW|), but stays within 1e-5 of the B12 sigma_W."""
+    rng = np.random.default_rng(41)
+    n = 4000
+    m_old = rng.uniform(-0.05, 0.05, n).astype(np.float32).astype(np.float64)
+    v_old = (m_old ** 2 * rng.uniform(1, 30, n)).astype(np.float32).astype(np.float64)
+    g = (-B1 / (1 - B1) * m_old * (1 + rng.uniform(-1e-4, 1e-4, n))).astype(np.float32).astype(np.float64)
+    W0 = rng.uniform(-1e-5, 1e-5, n).astype(np.float32).astype(np.float64)
+    shards = [W0.reshape(n, 1).copy()]
+    m, v = [m_old.reshape(n, 1).copy()], [v_old.reshape(n, 1).copy()]
+    ids = [np.arange(n)]
+    res = exchange.simulate_iteration(shards, ids, [g.reshape(n, 1)], None, 3, "coal", "fp64",
+                                      exchange.OptimConfig("adam", lr=1e-3, grad_scale=1.0), m, v)
+    a3 = 1e-3 * np.sqrt(1 - B2 ** 3) / (1 - B1 ** 3)
+    gpu = np.array([_adam_fp32_like_gpu(W0[i], m_old[i], v_old[i], g[i], a3)[0] for i in range(n)])
+    ref = shards[0][:, 0]
+    err_new = np.abs(gpu - ref) / np.maximum(np.abs(ref), res.sigma_W[:, 0])
+    err_old = np.abs(gpu - ref) / np.maximum(np.abs(ref), np.abs(W0) + np.abs(ref - W0))
+    assert err_new.max() <= 1e-5
+    assert err_old.max() > 1e-5
 
 
 def test_metric_helpers():
