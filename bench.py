@@ -943,6 +943,43 @@ def main():
     k_prof = kk
     kk += P
 
+    # ---------------- the same per-kernel events INSIDE a CUDA graph of the timed step: the library
+    # records its profiling events as event-record nodes while the stream is captured, so each
+    # kernel is timed in the graph structure `value` is measured with (no eager launch path, no host
+    # gaps; the event nodes only cut the PDL overlap next to each kernel).  The last of 3 replays
+    # is read.  This is the `roofline` timing; the eager pass above stays in `kernels`.
+    gprof = None
+    if graph is not None:
+        for j in range((k0 - kk) % nb):
+            step(kk + j)
+        kk += (k0 - kk) % nb
+        E.emb_join(ex.ctx, stream)
+        torch.cuda.synchronize()
+        try:
+            g2 = torch.cuda.CUDAGraph()
+            cap2 = torch.cuda.Stream()
+            cap2.wait_stream(stream)
+            E.emb_profile(ex.ctx, True)
+            with torch.cuda.graph(g2, stream=cap2):
+                for j in range(nb):
+                    b = (kk + j) % nb
+                    E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], cap2)
+                    E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], cap2)
+                    E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], cap2)
+                E.emb_join(ex.ctx, cap2)
+            E.emb_profile(ex.ctx, False)
+            stream.wait_stream(cap2)
+            for _ in range(3):
+                g2.replay()
+            torch.cuda.synchronize()
+            gprof = E.emb_profile_read(ex.ctx)
+            del g2
+            check_err("in-graph profile")
+        except Exception as e:  # pragma: no cover
+            E.emb_profile(ex.ctx, False)
+            print(f"[bench] in-graph kernel profile failed: {e}", file=sys.stderr)
+            gprof = None
+
     # algorithmic bytes per kernel, averaged over the profiled batches
     alg = {}
     for j in range(P):
@@ -958,6 +995,11 @@ def main():
         hb, nv = alg.get(kname, (0, 0))
         kern[kname] = {"avg_us": round(avg_us, 3), "launches": cnt, "hbm_bytes": int(hb), "nvlink_bytes": int(nv),
                        "hbm_gbs": round(hb / (avg_us * 1e-6) / 1e9, 1) if avg_us > 0 else None}
+        if gprof and kname in gprof and gprof[kname][1] > 0:
+            gus = gprof[kname][0] / gprof[kname][1] * 1e3
+            kern[kname]["avg_us_in_graph"] = round(gus, 3)
+            kern[kname]["hbm_gbs_in_graph"] = round(hb / (gus * 1e-6) / 1e9, 1) if gus > 0 else None
+    timing_note = "eager pass, CUDA events around each launch on its own stream"
     # dominant kernel: the one that must move the most algorithmic bytes
     dom = max(kern, key=lambda k: kern[k]["hbm_bytes"] + kern[k]["nvlink_bytes"])
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -965,14 +1007,20 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     nvl_peak = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
     dk = kern[dom]
-    nvl_gbs = dk["nvlink_bytes"] / (dk["avg_us"] * 1e-6) / 1e9 if dk["avg_us"] > 0 else 0
-    hbm_gbs = dk["hbm_gbs"] or 0
+    dom_us = dk["avg_us"]
+    if dk.get("avg_us_in_graph"):
+        dom_us = dk["avg_us_in_graph"]
+        timing_note = (f"CUDA events recorded as event-record nodes around each launch inside a CUDA graph of {nb} "
+                       "steps (the timed step's structure, last of 3 replays); eager-pass value in kernels.avg_us")
+    nvl_gbs = dk["nvlink_bytes"] / (dom_us * 1e-6) / 1e9 if dom_us > 0 else 0
+    hbm_gbs = dk["hbm_bytes"] / (dom_us * 1e-6) / 1e9 if dom_us > 0 else 0
     bound = "hbm" if (hbm_gbs / hbm_peak) >= (nvl_gbs / nvl_peak) or world == 1 else "nvlink"
     roof = {"bound": bound, "kernel": dom,
             "achieved": round(hbm_gbs if bound == "hbm" else nvl_gbs, 1),
             "peak": hbm_peak if bound == "hbm" else nvl_peak, "unit": "GB/s",
             "frac": round((hbm_gbs / hbm_peak) if bound == "hbm" else (nvl_gbs / nvl_peak), 4),
             "traffic": traffic_for(args.config, world, dom),
+            "avg_us": round(dom_us, 3), "timing": timing_note,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if bound == "hbm" else
             "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
 

@@ -289,9 +289,11 @@ emb_status emb_flush(emb_ctx* ctx, emb_stream_t stream);
 emb_status emb_join(emb_ctx* ctx, emb_stream_t stream);
 
 /* Per-kernel CUDA-event timing: when enabled, every kernel launch is
- * bracketed by events on its own stream.  emb_profile_read synchronises,
- * returns the summed milliseconds and launch counts per emb_kernel_kind
- * (arrays of EMB_NUM_KERNELS), and clears the record.                       */
+ * bracketed by events on its own stream (while the stream is being captured
+ * into a CUDA graph the events become event-record nodes, re-recorded by every
+ * replay).  emb_profile_read synchronises, returns the summed milliseconds and
+ * launch counts per emb_kernel_kind (arrays of EMB_NUM_KERNELS) — for a
+ * captured graph, of its last replay — and clears the record.              */
 emb_status emb_profile(emb_ctx* ctx, int32_t enable);
 emb_status emb_profile_read(emb_ctx* ctx, double* ms, int64_t* count);
 

@@ -153,18 +153,29 @@ struct emb_ctx {
 
 // Launch one kernel through `fn`, counting it and (when profiling) bracketing
 // it with CUDA events on its own stream.
+// While the stream is being captured into a CUDA graph the events become
+// event-record NODES (cudaEventRecordExternal): every replay re-records them,
+// so the kernel is timed inside the graph it is benchmarked in (no host gaps,
+// no eager launch path; the event nodes only cut the PDL overlap around it).
+static void prof_record(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  else cudaEventRecord(ev, s);
+}
+
 template <typename F>
 static cudaError_t run_k(emb_ctx* ctx, int kind, cudaStream_t s, F&& fn) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (ctx->prof) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    cudaEventRecord(a, s);
+    prof_record(a, s);
   }
   cudaError_t e = fn();
   ctx->launches += 1;
   if (ctx->prof) {
-    cudaEventRecord(b, s);
+    prof_record(b, s);
     ctx->prof_recs.push_back({kind, a, b});
   }
   return e;
