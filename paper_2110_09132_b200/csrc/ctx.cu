@@ -276,6 +276,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   // tuning knobs (measured defaults): forward grid cap per SM,
   // and how a prefetched N == 1 forward orders itself after its sort
   ctx->lc.fwd_per_sm = env_int("EMB_FWD_GRID_PER_SM", 4, 1, 32);
+  ctx->lc.reduce_per_sm = env_int("EMB_REDUCE_GRID_PER_SM", 12, 1, 32);
   ctx->sort_join = env_int("EMB_SORT_JOIN", 1, 0, 1) != 0;
   ctx->fwd_dedup1 = env_int("EMB_FWD_DEDUP1", 0, 0, 1) != 0;  // measured slower at N == 1 (profiles/r02_tune/next3.txt)
 

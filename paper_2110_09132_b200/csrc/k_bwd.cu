@@ -688,7 +688,7 @@ template <int DT>
 static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char* y, int p, int gate_flags,
                                  cudaStream_t s) {
   const int V = (c.cpr + 31) / 32;
-  const int ga = grid_for_warps(c.max_chunks, L.nsm * 12);
+  const int ga = grid_for_warps(c.max_chunks, L.nsm * L.reduce_per_sm);
   return EMB_LAUNCH_V(V, coal_reduce_kernel, DT, ga, 0, c, y, p, gate_flags);
 }
 

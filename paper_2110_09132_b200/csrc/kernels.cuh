@@ -7,6 +7,7 @@ namespace emb {
 struct LaunchCfg {
   int nsm;         // SM count of the device
   int fwd_per_sm;  // forward grid cap, CTAs per SM (env EMB_FWD_GRID_PER_SM, default 4)
+  int reduce_per_sm;  // coal_reduce grid cap, CTAs per SM (env EMB_REDUCE_GRID_PER_SM, default 12)
 };
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
