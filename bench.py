@@ -54,6 +54,9 @@ def parse():
                     help="NEXT-2: time an in-box baseline (baselines/inbox.py) instead of the exchange")
     ap.add_argument("--schedule", action="store_true",
                     help="NEXT-1: Computation Stall of FIFO / Horizontal / 2D scheduling (separate JSON line)")
+    ap.add_argument("--batch-mult", type=int, default=1,
+                    help="tokens per rank x M (sequences per rank, or max tokens when packed): the bandwidth-"
+                         "regime sweep of SURVEY §7 (cap 32768 tokens per rank)")
     ap.add_argument("--tables", type=int, default=1, choices=[1, 2],
                     help="NEXT-3: exchange this many stacked tables (same shape) in one call")
     ap.add_argument("--optim", default=None, choices=["sgd", "adam", "adagrad"],
@@ -743,6 +746,10 @@ def main():
     if world != args.gpus:
         world = args.gpus if world == 1 else world
     cfg = get_config(args.config)
+    if args.batch_mult > 1:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, **({"seq_len": cfg.seq_len * args.batch_mult} if cfg.packed
+                                          else {"batch": cfg.batch * args.batch_mult}))
     if args.optim:
         import dataclasses
         cfg = dataclasses.replace(cfg, optim=args.optim, lr=cfg.lr if args.optim == "adam" else 1e-2)

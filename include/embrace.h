@@ -87,7 +87,7 @@ typedef struct {
   int32_t rank;         /* r, 0..N-1                                                */
   int32_t device;       /* CUDA device ordinal of this rank                         */
   emb_dtype dtype;      /* storage / wire / output dtype; math is fp32              */
-  int32_t max_tokens;   /* capacity: tokens per rank per iteration                  */
+  int32_t max_tokens;   /* capacity: tokens per rank per iteration, 1..32768         */
   emb_bwd_mode mode;
   emb_optim optim;
   float lr, beta1, beta2, eps;

@@ -50,7 +50,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (cfg->world < 1 || cfg->world > EMB_MAX_WORLD) return EMB_ERR_SHAPE;
   if (cfg->rank < 0 || cfg->rank >= cfg->world) return EMB_ERR_INVALID_ARG;
   if (cfg->vocab < 1 || cfg->vocab >= (1ll << 30)) return EMB_ERR_INVALID_ARG;
-  if (cfg->dim < 1 || cfg->max_tokens < 1 || cfg->max_tokens > 16384) return EMB_ERR_CAPACITY;
+  if (cfg->dim < 1 || cfg->max_tokens < 1 || cfg->max_tokens > 32768) return EMB_ERR_CAPACITY;
   if (cfg->dtype != EMB_FP32 && cfg->dtype != EMB_BF16) return EMB_ERR_INVALID_ARG;
   if (cfg->mode < EMB_BWD_RAW || cfg->mode > EMB_BWD_SPLIT) return EMB_ERR_INVALID_ARG;
   if (cfg->optim != EMB_SGD && cfg->optim != EMB_ADAM && cfg->optim != EMB_ADAGRAD) return EMB_ERR_INVALID_ARG;

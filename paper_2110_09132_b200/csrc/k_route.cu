@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p, 
 // ============================================================== launchers
 static int ept_for(int max_tok) {
   const int need = (max_tok + RT_THREADS - 1) / RT_THREADS;
-  const int opts[] = {1, 2, 4, 5, 8, 12, 16};
+  const int opts[] = {1, 2, 4, 5, 8, 12, 16, 32};  // 32: up to 32768 uniques (the 16-CTA sort's cap)
   for (int e : opts)
     if (e >= need) return e;
   return -1;
@@ -287,6 +287,7 @@ static void* tables_fn(int ept) {
     case 8: return (void*)tables_kernel<8>;
     case 12: return (void*)tables_kernel<12>;
     case 16: return (void*)tables_kernel<16>;
+    case 32: return (void*)tables_kernel<32>;
   }
   return nullptr;
 }
@@ -319,7 +320,8 @@ cudaError_t preload_route() {
   for (const void* f : {(const void*)markpush_kernel, (const void*)marktag_kernel, (const void*)plan_kernel,
                         (const void*)tables_kernel<1>, (const void*)tables_kernel<2>,
                         (const void*)tables_kernel<4>, (const void*)tables_kernel<5>, (const void*)tables_kernel<8>,
-                        (const void*)tables_kernel<12>, (const void*)tables_kernel<16>})
+                        (const void*)tables_kernel<12>, (const void*)tables_kernel<16>,
+                        (const void*)tables_kernel<32>})
     if (cudaError_t e = preload(f)) return e;
   return cudaSuccess;
 }

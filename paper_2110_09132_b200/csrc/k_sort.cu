@@ -7,11 +7,12 @@
 // source n, the ascending unique ids and the positions of each id in
 // ascending position order (reading R12: canonical summation order).
 //
-// B200 design (DESIGN.md §5 "sort_unique").  A batch of up to 16384 keys is
+// B200 design (DESIGN.md §5 "sort_unique").  A batch of up to 32768 keys is
 // too little work for 148 SMs and too much for one: one SM needed 22 us (LM)
 // to 62 us (BERT), enough to bound the whole step from the auxiliary stream.
-// Here a cluster of CL = 8 CTAs shares one source's keys through distributed
-// shared memory (DSMEM):
+// Here a cluster of CL = 8 (<= 16384 keys) or 16 (<= 32768 keys, non-portable
+// size) CTAs shares one source's keys through distributed shared memory
+// (DSMEM):
 //   keys   (id' << posbits) | pos with id' = L for dropped tokens (pad when
 //          pad_id >= 0, out-of-range ids), so dropped keys sort last; a
 //          stable LSD radix sort over the id bits only (8-bit digits: LM 3
@@ -28,6 +29,7 @@
 // Nine cluster barriers per sort (LM), no global atomics, deterministic.
 #include <cooperative_groups.h>
 #include <stddef.h>
+#include <stdlib.h>
 
 #include "kernels.cuh"
 
@@ -35,14 +37,21 @@ namespace cg = cooperative_groups;
 
 namespace emb {
 
-static constexpr int CL = 8;           // CTAs per cluster (portable size)
-static constexpr int CS_THREADS = 256;
-static constexpr int CS_WARPS = CS_THREADS / 32;
+// Two shapes of the same kernel, 256 threads per CTA: a cluster of 8 CTAs
+// (portable size) per source for batches up to 16384 keys, or of 16 CTAs
+// (non-portable cluster size, opt-in) up to 32768 keys — the tokens-per-rank
+// cap of the exchange.  (A single 1024-thread CTA per source was measured
+// slower: profiles/r02_tune/sort_join.txt.)
+static constexpr int CL8 = 8;
+static constexpr int CL16 = 16;
+static constexpr int TH8 = 256;
 static constexpr int NB = 256;         // bins of an 8-bit digit
 static constexpr int DB = 8;
 
-// Exclusive scan of one int per thread over the CTA (CS_THREADS); *total gets the sum.
+// Exclusive scan of one int per thread over the CTA (TH threads); *total gets the sum.
+template <int TH>
 __device__ __forceinline__ int cta_exscan(int v, int* tmp, int* total) {
+  constexpr int CS_WARPS = TH / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
@@ -65,6 +74,7 @@ __device__ __forceinline__ int cta_exscan(int v, int* tmp, int* total) {
 }
 
 // Sum of `v` over the cluster's CTAs with rank < cr (exclusive) and over all.
+template <int CL>
 __device__ __forceinline__ void cluster_exsum(cg::cluster_group& cluster, int* slot, int cr, int* before, int* all) {
   int b = 0, a = 0;
 #pragma unroll
@@ -77,9 +87,10 @@ __device__ __forceinline__ void cluster_exsum(cg::cluster_group& cluster, int* s
   *all = a;
 }
 
-template <typename K, int EPT>
+template <typename K, int EPT, int CL, int CS_THREADS>
 __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, const int* own_ids, int own_n,
                                                              int from_bwd) {
+  constexpr int CS_WARPS = CS_THREADS / 32;
   EMB_TR_ENTRY();
   pdl_wait();
   cg::cluster_group cluster = cg::this_cluster();
@@ -173,9 +184,9 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
       }
     }
     __syncthreads();
-    {  // digit d = tid: exclusive offsets over warps, CTA total
+    if (tid < NB) {  // digit d = tid: exclusive offsets over warps, CTA total
       int run = 0;
-#pragma unroll
+#pragma unroll 8
       for (int ww = 0; ww < CS_WARPS; ++ww) {
         const int x = wh[ww][tid];
         wh[ww][tid] = run;
@@ -185,10 +196,10 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     }
     cluster.sync();  // every CTA's ch[] is complete
     {
-      int pre, tot, all;
-      cluster_exsum(cluster, &ch[tid], cr, &pre, &tot);
-      const int ex = cta_exscan(tot, tmp, &all);
-      gs[tid] = ex + pre;
+      int pre = 0, tot = 0, all;
+      if (tid < NB) cluster_exsum<CL>(cluster, &ch[tid], cr, &pre, &tot);
+      const int ex = cta_exscan<CS_THREADS>(tot, tmp, &all);
+      if (tid < NB) gs[tid] = ex + pre;
     }
     __syncthreads();
 #pragma unroll
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   }
   {
     int tk_all;
-    cta_exscan(lane == 0 ? kept_tok : 0, tmp, &tk_all);
+    cta_exscan<CS_THREADS>(lane == 0 ? kept_tok : 0, tmp, &tk_all);
     if (tid == 0) xs[1] = tk_all;
   }
   __syncthreads();
@@ -252,8 +263,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   }
   cluster.sync();  // xs[0] (kept heads), xs[1] (kept tokens), xs[4] (first kept head) of every CTA
   int kb, U, tkb, Tk;
-  cluster_exsum(cluster, &xs[0], cr, &kb, &U);
-  cluster_exsum(cluster, &xs[1], cr, &tkb, &Tk);
+  cluster_exsum<CL>(cluster, &xs[0], cr, &kb, &U);
+  cluster_exsum<CL>(cluster, &xs[1], cr, &tkb, &Tk);
   (void)tkb;
   int next_first = Tk;  // end of this CTA's last segment: the next kept head, else the first dropped key
   for (int q = CL - 1; q > cr; --q) {
@@ -309,14 +320,14 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   }
   {
     int a, b;
-    cta_exscan(my_ch, tmp, &a);
-    cta_exscan(my_long, tmp, &b);
+    cta_exscan<CS_THREADS>(my_ch, tmp, &a);
+    cta_exscan<CS_THREADS>(my_long, tmp, &b);
     if (tid == 0) { xs[2] = a; xs[3] = b; xs[5] = 0; }
   }
   cluster.sync();
   int cb, NCH, lb, NLONG;
-  cluster_exsum(cluster, &xs[2], cr, &cb, &NCH);
-  cluster_exsum(cluster, &xs[3], cr, &lb, &NLONG);
+  cluster_exsum<CL>(cluster, &xs[2], cr, &cb, &NCH);
+  cluster_exsum<CL>(cluster, &xs[3], cr, &lb, &NLONG);
   constexpr int QMAX = 32, QMIN = 8;  // uniques of > QMIN chunks: descriptors written by the whole CTA
   __shared__ int4 lq[QMAX];
   __shared__ int lq_off[QMAX];
@@ -330,8 +341,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
       nch = (b - a + c.C - 1) / c.C;
     }
     int tch, tlong;
-    const int och = cta_exscan(nch, tmp, &tch);
-    const int olong = cta_exscan(nch > 1 ? 1 : 0, tmp, &tlong);
+    const int och = cta_exscan<CS_THREADS>(nch, tmp, &tch);
+    const int olong = cta_exscan<CS_THREADS>(nch > 1 ? 1 : 0, tmp, &tlong);
     if (j < hc) {
       const int off = cb + och;
       chunk_off[k] = off;
@@ -385,9 +396,14 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   pdl_trigger();
 }
 
+// Shape choice: the 8-CTA cluster up to 8 x 2048 keys per source, the 16-CTA
+// cluster above (up to 16 x 2048).
+static int sort_cl(int max_tok) { return max_tok <= CL8 * 8 * TH8 ? CL8 : CL16; }
+
 static int cs_ept(int max_tok) {
-  const int per = (max_tok + CL - 1) / CL;
-  const int need = (per + CS_THREADS - 1) / CS_THREADS;
+  const int cl = sort_cl(max_tok);
+  const int per = (max_tok + cl - 1) / cl;
+  const int need = (per + TH8 - 1) / TH8;
   const int opts[] = {1, 2, 3, 4, 6, 8};
   for (int e : opts)
     if (e >= need) return e;
@@ -397,43 +413,54 @@ static int cs_ept(int max_tok) {
 size_t sort_smem_bytes(int max_tok, bool key64) {
   const int e = cs_ept(max_tok);
   if (e < 0) return (size_t)1 << 30;
-  return (size_t)2 * e * CS_THREADS * (key64 ? 8 : 4);
+  return (size_t)2 * e * TH8 * (key64 ? 8 : 4);
 }
 
-template <typename K>
-static void* csort_fn(int ept) {
+template <typename K, int CL>
+static void* csort_fn_shape(int ept) {
   switch (ept) {
-    case 1: return (void*)csort_kernel<K, 1>;
-    case 2: return (void*)csort_kernel<K, 2>;
-    case 3: return (void*)csort_kernel<K, 3>;
-    case 4: return (void*)csort_kernel<K, 4>;
-    case 6: return (void*)csort_kernel<K, 6>;
-    case 8: return (void*)csort_kernel<K, 8>;
+    case 1: return (void*)csort_kernel<K, 1, CL, TH8>;
+    case 2: return (void*)csort_kernel<K, 2, CL, TH8>;
+    case 3: return (void*)csort_kernel<K, 3, CL, TH8>;
+    case 4: return (void*)csort_kernel<K, 4, CL, TH8>;
+    case 6: return (void*)csort_kernel<K, 6, CL, TH8>;
+    case 8: return (void*)csort_kernel<K, 8, CL, TH8>;
     default: return nullptr;
   }
 }
 
+template <typename K>
+static void* csort_fn(int max_tok) {
+  const int e = cs_ept(max_tok);
+  return sort_cl(max_tok) == CL8 ? csort_fn_shape<K, CL8>(e) : csort_fn_shape<K, CL16>(e);
+}
+
 cudaError_t sort_set_smem(int max_tok, bool key64, size_t smem) {
-  void* f = key64 ? csort_fn<unsigned long long>(cs_ept(max_tok)) : csort_fn<uint32_t>(cs_ept(max_tok));
+  void* f = key64 ? csort_fn<unsigned long long>(max_tok) : csort_fn<uint32_t>(max_tok);
   if (!f) return cudaErrorInvalidValue;
+  if (sort_cl(max_tok) == CL16) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   if (smem > 48 * 1024) return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return cudaSuccess;
 }
 
 cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, int from_bwd, bool key64,
                         size_t smem, cudaStream_t s) {
-  void* f = key64 ? csort_fn<unsigned long long>(cs_ept(c.max_tok)) : csort_fn<uint32_t>(cs_ept(c.max_tok));
+  void* f = key64 ? csort_fn<unsigned long long>(c.max_tok) : csort_fn<uint32_t>(c.max_tok);
   if (!f) return cudaErrorInvalidValue;
+  const int cl = sort_cl(c.max_tok);
   DevCtx cc = c;
   void* args[] = {&cc, &p, &own_ids, &own_n, &from_bwd};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c.N * CL);
-  cfg.blockDim = dim3(CS_THREADS);
+  cfg.gridDim = dim3(c.N * cl);
+  cfg.blockDim = dim3(TH8);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -445,8 +472,9 @@ cudaError_t launch_sort(const DevCtx& c, int p, const int* own_ids, int own_n, i
 
 cudaError_t preload_sort() {
   for (int e : {1, 2, 3, 4, 6, 8}) {
-    if (cudaError_t r = preload(csort_fn<uint32_t>(e))) return r;
-    if (cudaError_t r = preload(csort_fn<unsigned long long>(e))) return r;
+    for (void* f : {csort_fn_shape<uint32_t, CL8>(e), csort_fn_shape<unsigned long long, CL8>(e),
+                    csort_fn_shape<uint32_t, CL16>(e), csort_fn_shape<unsigned long long, CL16>(e)})
+      if (cudaError_t r = preload(f)) return r;
   }
   return cudaSuccess;
 }

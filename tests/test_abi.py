@@ -50,7 +50,7 @@ def test_host_validation(E):
         (E.make_config(1000, 4, world=8), "EMB_ERR_SHAPE"),        # N > D... and N > 8 rejected below
         (E.make_config(1000, 16, world=2, rank=2), "EMB_ERR_INVALID_ARG"),
         (E.make_config(1000, 16, max_tokens=0), "EMB_ERR_CAPACITY"),
-        (E.make_config(1000, 16, max_tokens=20000), "EMB_ERR_CAPACITY"),
+        (E.make_config(1000, 16, max_tokens=40000), "EMB_ERR_CAPACITY"),  # cap 32768 (16-CTA sort)
         (E.make_config(0, 16), "EMB_ERR_INVALID_ARG"),
     ]
     for cfg, want in bad:

@@ -104,3 +104,7 @@ def test_two_tables_colocated():
     cfg = Config("twotab", 1000, 64, "bf16", 8, 16, 8, optim="adam", lr=1e-2)
     parity_run(cfg, N=2, mode="split", iters=3, ids_override=_two_tables(600), table_rows=(600, 400),
                prefetch=True, colocated=True)
+
+
+def test_batch_above_16k_colocated():
+    parity_run(_small("transformer", 600), N=2, mode="split", iters=2, prefetch=True, colocated=True)

@@ -245,3 +245,12 @@ def test_forward_dedup_n1_knob(monkeypatch):
     monkeypatch.setenv("EMB_FWD_DEDUP1", "1")
     parity_run(get_config("tiny"), N=1, mode="split", iters=4, prefetch=True)
     parity_run(_small("lstm_lm", batch=8), N=1, mode="split", iters=3, prefetch=True, rows_sample=512)
+
+
+# ---------------------------------------------------------------- tokens per rank above 16384 (16-CTA sort)
+
+def test_batch_above_16k_tokens():
+    """max_tokens up to 32768 (the 16-CTA cluster sort): GNMT shape with 8x its
+    batch (26,624 tokens per rank) and an LM-vocabulary fp32 case."""
+    parity_run(dataclasses.replace(get_config("gnmt"), batch=1024), N=1, mode="split", iters=2, prefetch=True)
+    parity_run(dataclasses.replace(get_config("lstm_lm"), batch=512), N=1, mode="coal", iters=2, rows_sample=1024)
