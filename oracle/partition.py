@@ -69,3 +69,38 @@ def request_counts_rowwise(tokens, L, N):
     of PAPER.md:272-273)."""
     tokens = np.asarray(tokens, dtype=np.int64)
     return [int(((tokens >= a) & (tokens < b)).sum()) for (a, b) in row_ranges(L, N)]
+
+
+def request_counts_rowwise_hashed(tokens, N):
+    """Row-wise partition with rows dealt round-robin (owner = id mod N), the
+    usual fix for frequency-sorted vocabularies; still imbalanced when a few
+    ids dominate."""
+    tokens = np.asarray(tokens, dtype=np.int64)
+    return [int((tokens % N == s).sum()) for s in range(N)]
+
+
+def forward_bytes_out(ids_all, L, D, N, scheme, esz=4):
+    """NVLink bytes each owner s SENDS in one forward exchange (the lookup
+    results other ranks need), self-delivery excluded:
+      column-wise  every owner sends every other rank's tokens, d = D/N columns:
+                   (T - T_s) * (D/N) * e  (balanced, PAPER.md:274);
+      row / hash   owner s sends full rows for the tokens of other ranks that
+                   fall in its rows: count_{r != s}(ids_r owned by s) * D * e."""
+    T = [int(np.asarray(x).size) for x in ids_all]
+    if scheme == "column":
+        d = D // N
+        return [(sum(T) - T[s]) * d * esz for s in range(N)]
+    out = []
+    for s in range(N):
+        c = 0
+        for r in range(N):
+            if r == s:
+                continue
+            if scheme == "row":
+                c += request_counts_rowwise(ids_all[r], L, N)[s]
+            elif scheme == "hash":
+                c += request_counts_rowwise_hashed(ids_all[r], N)[s]
+            else:
+                raise ValueError(scheme)
+        out.append(c * D * esz)
+    return out

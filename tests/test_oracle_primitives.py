@@ -395,3 +395,35 @@ def test_adagrad_exchange_equals_dense_reference(mode):
         exchange.dense_reference(Wd, wl.ids[k], wl.dY[k], k + 1, "fp64", opt, sd, None)
     np.testing.assert_allclose(np.hstack(shards), Wd, rtol=0, atol=1e-12)
     np.testing.assert_allclose(np.hstack(s_sh), sd, rtol=1e-12, atol=1e-14)
+
+
+# ---------------------------------------------------------------- NEXT-4: row-wise partition (load-imbalance study)
+
+def test_rowwise_vs_columnwise_requests_worked_example():
+    """row-wise shards get unequal request counts when word
+    frequencies differ; column-wise shards all serve every request."""
+    from oracle import partition
+    toks = np.array([0, 0, 0, 1, 5])
+    assert partition.request_counts_rowwise(toks, 6, 2) == [4, 1]          # rows [0,3) and [3,6)
+    assert partition.request_counts_rowwise_hashed(toks, 2) == [3, 2]      # even / odd ids
+    assert partition.request_counts_columnwise(toks, 2) == [5, 5]
+    ids_all = [np.array([0, 0, 1]), np.array([0, 5])]
+    # column: owner 0 sends rank 1's 2 tokens, owner 1 sends rank 0's 3 tokens, D/N = 2 columns of 4 B
+    assert partition.forward_bytes_out(ids_all, 6, 4, 2, "column") == [2 * 2 * 4, 3 * 2 * 4]
+    # row: owner 0 (rows 0..2) sends rank 1's id 0; owner 1 (rows 3..5) sends nothing of rank 0's
+    assert partition.forward_bytes_out(ids_all, 6, 4, 2, "row") == [1 * 4 * 4, 0]
+
+
+def test_rowwise_imbalance_on_zipf_batches():
+    """On Zipf-distributed (frequency-sorted) ids the most loaded row-wise owner
+    serves far more than the mean, column-wise owners exactly the mean."""
+    from oracle import partition
+    from synthetic import get_config, make_workload
+    cfg = get_config("gnmt")
+    N = 4
+    wl = make_workload(cfg, N, 1, with_dY=False)
+    ids = wl.ids[0]
+    col = partition.forward_bytes_out(ids, cfg.L, cfg.D, N, "column", 2)
+    row = partition.forward_bytes_out(ids, cfg.L, cfg.D, N, "row", 2)
+    assert max(col) / (sum(col) / N) < 1.01
+    assert max(row) / (sum(row) / N) > 2.0
