@@ -434,8 +434,12 @@ def run_dense(args, cfg, world, rank, local):
     prios = list(range(nblk))[::-1]          # enqueued in BP order: the last layer (largest FP index) first
     last = []
 
-    def sparse(k):
-        b = k % nb
+    seq = [0]  # global step counter: the batch sequence continues across the timed phases (each forward
+               # must see the ids the previous backward promised)
+
+    def sparse(_k):
+        b = seq[0] % nb
+        seq[0] += 1
         E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], stream)
         E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], stream)
         E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], stream)
