@@ -277,6 +277,14 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   // and how a prefetched N == 1 forward orders itself after its sort
   ctx->lc.fwd_per_sm = env_int("EMB_FWD_GRID_PER_SM", 4, 1, 32);
   ctx->lc.reduce_per_sm = env_int("EMB_REDUCE_GRID_PER_SM", 12, 1, 32);
+  // N == 1 forward via the bulk-copy engine for tables larger than L2 (rows come
+  // from HBM: LM 19.4 vs 19.8 us); for the 32K-row tables, which live in L2,
+  // the register gather measured faster (GNMT 19.1 vs 19.6, BERT 44.6 vs 46.4 us;
+  // profiles/r02_tune/fwd_bulk.txt).  EMB_FWD_BULK=0/1 overrides.
+  {
+    const bool big = (double)cfg->vocab * cfg->dim * pl.esz > 96.0 * (1 << 20);
+    ctx->lc.fwd_bulk = env_int("EMB_FWD_BULK", big ? 1 : 0, 0, 1);
+  }
   ctx->sort_join = env_int("EMB_SORT_JOIN", 1, 0, 1) != 0;
   ctx->fwd_dedup1 = env_int("EMB_FWD_DEDUP1", 0, 0, 1) != 0;  // measured slower at N == 1 (profiles/r02_tune/next3.txt)
 
@@ -342,6 +350,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   }
 #undef ALLOC
   if (sort_set_smem(cfg->max_tokens, pl.key64, pl.sort_smem) != cudaSuccess) goto fail;
+  if (fwd_bulk_set_smem(ctx->dc) != cudaSuccess) goto fail;
   // load every kernel now (see kernels.cuh: preload)
   if (preload_fwd() != cudaSuccess || preload_bwd() != cudaSuccess || preload_route() != cudaSuccess ||
       preload_sort() != cudaSuccess || preload_gate() != cudaSuccess)

@@ -179,8 +179,158 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
   pdl_trigger();
 }
 
+// ------------------------------------------------------------------ N == 1: bulk-copy (TMA) gather
+// With one process the whole row lives in this GPU's shard, so the gather is a
+// row copy W[id] -> Y[j].  fwd_bulk moves rows with the Blackwell bulk-copy
+// engine instead of registers: a CTA stages R rows per stage in shared memory
+// (cp.async.bulk global -> shared, one 16-byte-multiple row per lane of warp 0,
+// completion counted on an mbarrier), then writes them out with
+// cp.async.bulk shared -> global; two stages, so the loads of batch i+1 are in
+// flight while batch i drains.  Invalid ids get a zero row (generic stores)
+// and the sticky ERR_ID, as in fwd_kernel.
+static constexpr int FB_THREADS = 128;
+static constexpr int FB_STAGES = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int NG>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NG) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(FB_THREADS) fwd_bulk_kernel(DevCtx c, const int* __restrict__ ids, int n,
+                                                             char* __restrict__ out, int p, int prefetched, int R) {
+  EMB_TR_ENTRY();
+  extern __shared__ __align__(128) unsigned char fb_smem[];
+  __shared__ __align__(8) uint64_t bars[FB_STAGES];
+  pdl_wait();
+  const uint32_t t = c.t_rec[p ^ 1] + 1;
+  EMB_TR_BEGIN(0, t);
+  EMB_TR_WAITED(0, t);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nth = gridDim.x * blockDim.x;
+  if (tid == 0) {  // the forward's per-iteration bookkeeping (as fwd_kernel)
+    c.t_rec[p] = t;
+    if (c.optim == ADAM) {
+      const double td = (double)t;
+      c.alpha[p] = (float)((double)c.lr * sqrt(1.0 - pow((double)c.beta2, td)) / (1.0 - pow((double)c.beta1, td)));
+    }
+    atomicAdd(&c.stats[0], (unsigned long long)n * c.d * c.esz);
+  }
+  if (!prefetched) {  // (a1) at N == 1: the ids are this rank's own gathered batch
+    for (int j = tid; j < n; j += nth) gids_of(c, 0, p, 0)[j] = ids[j];
+    if (tid == 0) {
+      *ntok_of(c, 0, p, 0) = n;
+      atomicAdd(&c.stats[2], (unsigned long long)n * 4ull);
+    }
+  } else {  // prefetch check: fingerprint of the ids the sort read (k_gate.cu / k_bwd.cu compare)
+    unsigned h = 0;
+    for (int j = tid; j < n; j += nth) h += prefetch_hash(__ldg(ids + j), j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0 && h) atomicAdd(&c.fp[p * 4 + 0], h);
+    if (tid == 0) atomicAdd(&c.fp[p * 4 + 1], (unsigned)n);
+  }
+  const uint32_t rowB = (uint32_t)c.D * c.esz;
+  const char* shard = shard_of(c, 0);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < FB_STAGES; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int it = 0;
+  for (int j0 = blockIdx.x * R; j0 < n; j0 += gridDim.x * R, ++it) {
+    const int st = it & (FB_STAGES - 1);
+    const uint32_t par = (uint32_t)(it / FB_STAGES) & 1u;
+    unsigned char* buf = fb_smem + (size_t)st * R * rowB;
+    if (w == 0) {
+      // the stage's previous bulk stores (issued FB_STAGES batches ago by this
+      // warp) must have finished reading its shared memory
+      if (it >= FB_STAGES) bulk_wait_read<FB_STAGES - 1>();
+      __syncwarp();
+      const int j = j0 + lane;
+      const bool valid = lane < R && j < n;
+      const int id = valid ? __ldg(ids + j) : 0;
+      const bool ok = valid && (unsigned)id < (unsigned long long)c.L;
+      const unsigned okm = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) mbar_expect_tx(&bars[st], (uint32_t)__popc(okm) * rowB);
+      __syncwarp();
+      if (ok) bulk_load(buf + (size_t)lane * rowB, shard + (size_t)id * rowB, rowB, &bars[st]);
+      if (valid && !ok) {  // invalid id: zero row, sticky error
+        atomicOr(c.err, ERR_ID);
+        for (uint32_t o = 0; o < rowB; o += 16) st16(out + (size_t)j * rowB + o, make_uint4(0, 0, 0, 0));
+      }
+      mbar_wait(&bars[st], par);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (ok) bulk_store(out + (size_t)j * rowB, buf + (size_t)lane * rowB, rowB);
+      bulk_commit();
+    }
+  }
+  if (w == 0) bulk_wait_all();  // Y complete before the grid completes (the next kernel reads it)
+  EMB_TR_END(0, t);
+  pdl_trigger();
+}
+
+#ifndef EMB_FWD_BULK_ROWS
+#define EMB_FWD_BULK_ROWS 16
+#endif
+#ifndef EMB_FWD_BULK_PER_SM
+#define EMB_FWD_BULK_PER_SM 3
+#endif
+static int fwd_bulk_rows(const DevCtx& c) {
+  int R = EMB_FWD_BULK_ROWS;  // rows per stage (one per lane of warp 0)
+  while (R > 1 && (size_t)FB_STAGES * R * c.D * c.esz > 128 * 1024) R >>= 1;
+  return R;
+}
+
+cudaError_t fwd_bulk_set_smem(const DevCtx& c) {
+  const size_t smem = (size_t)FB_STAGES * fwd_bulk_rows(c) * c.D * c.esz;
+  return cudaFuncSetAttribute((const void*)fwd_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int n, void* out, int p,
                        int prefetched, int dedup, cudaStream_t s) {
+  if (c.N == 1 && dedup == 0 && L.fwd_bulk) {
+    const int R = fwd_bulk_rows(c);
+    int grid = (n + R - 1) / R;
+    if (grid > L.nsm * EMB_FWD_BULK_PER_SM) grid = L.nsm * EMB_FWD_BULK_PER_SM;
+    if (grid < 1) grid = 1;
+    const size_t smem = (size_t)FB_STAGES * R * c.D * c.esz;
+    return launch_pdl(fwd_bulk_kernel, dim3(grid), dim3(FB_THREADS), smem, s, c, ids, n, static_cast<char*>(out), p,
+                      prefetched, R);
+  }
   const int warps = (n + FWD_ROWS - 1) / FWD_ROWS;
   int grid = (warps + FWD_THREADS / 32 - 1) / (FWD_THREADS / 32);
   if (grid < 1) grid = 1;
@@ -197,7 +347,7 @@ cudaError_t launch_fwd(const DevCtx& c, const LaunchCfg& L, const int* ids, int 
 
 cudaError_t preload_fwd() {
   for (const void* f : {(const void*)fwd_kernel<1>, (const void*)fwd_kernel<2>, (const void*)fwd_kernel<4>,
-                        (const void*)fwd_kernel<8>})
+                        (const void*)fwd_kernel<8>, (const void*)fwd_bulk_kernel})
     if (cudaError_t e = preload(f)) return e;
   return cudaSuccess;
 }

@@ -8,6 +8,7 @@ struct LaunchCfg {
   int nsm;         // SM count of the device
   int fwd_per_sm;  // forward grid cap, CTAs per SM (env EMB_FWD_GRID_PER_SM, default 4)
   int reduce_per_sm;  // coal_reduce grid cap, CTAs per SM (env EMB_REDUCE_GRID_PER_SM, default 12)
+  int fwd_bulk;       // N == 1 forward through the bulk-copy engine (env EMB_FWD_BULK)
 };
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
@@ -62,6 +63,7 @@ inline cudaError_t preload(const void* f) {
   return cudaFuncGetAttributes(&a, f);
 }
 cudaError_t preload_fwd();
+cudaError_t fwd_bulk_set_smem(const DevCtx& c);
 cudaError_t preload_bwd();
 cudaError_t preload_route();
 cudaError_t preload_sort();

@@ -247,6 +247,17 @@ def test_forward_dedup_n1_knob(monkeypatch):
     parity_run(_small("lstm_lm", batch=8), N=1, mode="split", iters=3, prefetch=True, rows_sample=512)
 
 
+@pytest.mark.parametrize("bulk", ["0", "1"])
+def test_forward_bulk_copy_knob(monkeypatch, bulk):
+    """EMB_FWD_BULK forces the N == 1 forward onto the bulk-copy (TMA) gather or
+    the register gather (default: bulk for tables > 96 MB).  Both exact, fp32
+    and bf16, ragged batch tails, with and without the prefetched sort."""
+    monkeypatch.setenv("EMB_FWD_BULK", bulk)
+    parity_run(get_config("tiny"), N=1, mode="split", iters=3, prefetch=False)
+    parity_run(_small("gnmt", batch=5), N=1, mode="split", iters=3, prefetch=True)
+    parity_run(_small("lstm_lm", batch=3), N=1, mode="coal", iters=2, prefetch=True, rows_sample=512)
+
+
 # ---------------------------------------------------------------- tokens per rank above 16384 (16-CTA sort)
 
 def test_batch_above_16k_tokens():
