@@ -57,6 +57,7 @@ struct DevCtx {
   int D, d, esz;          // esz: bytes per element of the table dtype
   int dtype, mode, optim;
   int max_tok;
+  int pdl_early;          // EMB_PDL_EARLY: compute kernels trigger their dependents right after griddepcontrol.wait
   int cpr, cps;           // 16-byte chunks per full row (D*esz/16) / per column slice (d*esz/16)
   long long pad_id;
   float lr, beta1, beta2, eps, scale;

@@ -297,6 +297,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   c.lr = cfg->lr; c.beta1 = cfg->beta1; c.beta2 = cfg->beta2; c.eps = cfg->eps;
   c.scale = cfg->grad_scale != 0.f ? cfg->grad_scale : 1.0f / (float)pl.N;
   c.timeout_ns = (unsigned long long)(cfg->timeout_ms > 0 ? cfg->timeout_ms : 10000) * 1000000ull;
+  c.pdl_early = env_int("EMB_PDL_EARLY", 0, 0, 1);
   c.C = pl.C; c.max_chunks = pl.max_chunks; c.max_long = pl.max_long; c.idbits = pl.idbits; c.posbits = pl.posbits;
   c.lay = pl.lay;
 

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
                                                                   int gate_flags) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   constexpr int EPV = Vec<DT>::EPV;
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
@@ -324,6 +325,7 @@ template <int DT>
 __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   constexpr int EPV = Vec<DT>::EPV;
   __shared__ __align__(16) float comb[BWD_WARPS][SLICE];  // warp partial sums of one column slice
   __shared__ __align__(16) float row[SLICE];              // combined slice
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
 __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const int r = c.r;
   const uint32_t t = c.t_rec[p];
   EMB_TR_BEGIN(5, t);
@@ -459,6 +462,7 @@ __global__ void __launch_bounds__(BWD_THREADS) defpush_kernel(DevCtx c, int p) {
 // ------------------------------------------------------------------ RAW mode
 __global__ void __launch_bounds__(BWD_THREADS) rawpush_kernel(DevCtx c, const char* __restrict__ dY, int n, int p) {
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const int r = c.r;
   const size_t row_bytes = (size_t)c.D * c.esz, slice_bytes = (size_t)c.d * c.esz;
   const size_t total = (size_t)n * c.cpr;
@@ -478,6 +482,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawpush_kernel(DevCtx c, const ch
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p) {
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   constexpr int EPV = Vec<DT>::EPV;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -511,6 +516,7 @@ __global__ void __launch_bounds__(BWD_THREADS) rawcoal_a_kernel(DevCtx c, int p)
 template <int DT, int V>
 __global__ void __launch_bounds__(BWD_THREADS) rawcoal_b_kernel(DevCtx c, int p) {
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   constexpr int EPV = Vec<DT>::EPV;
   extern __shared__ __align__(16) float wpart[];  // [BWD_WARPS][d]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -563,6 +569,7 @@ template <int DT, bool RAWSRC>
 __global__ void __launch_bounds__(BWD_THREADS) merge_kernel(DevCtx c, int p, int part, int G) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   constexpr int EPV = Vec<DT>::EPV;
   const uint32_t t = c.t_rec[p];
   (void)t;

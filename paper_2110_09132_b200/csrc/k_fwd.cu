@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
                                                           int dedup) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const uint32_t t = c.t_rec[p ^ 1] + 1;  // iteration number (device-resident, graph-replay safe)
   EMB_TR_BEGIN(0, t);
   EMB_TR_WAITED(0, t);
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(FB_THREADS) fwd_bulk_kernel(DevCtx c, const in
   extern __shared__ __align__(128) unsigned char fb_smem[];
   __shared__ __align__(8) uint64_t bars[FB_STAGES];
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const uint32_t t = c.t_rec[p ^ 1] + 1;
   EMB_TR_BEGIN(0, t);
   EMB_TR_WAITED(0, t);

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(MP_THREADS) markpush_kernel(DevCtx c, int p, c
                                                              int n_next, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   // t of this batch: N > 1 the sort of t precedes on this stream (DESIGN B7);
   // N == 1 (side stream) the side stream's own count of backward calls
   if (t_mode && blockIdx.x == 0 && threadIdx.x == 0) c.side_it[0] += 1;
@@ -99,6 +100,7 @@ static constexpr int MT_CTAS_PER_SRC = 8;
 __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, int do_mark, int set_flag, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const uint32_t t = t_mode ? __ldcg(c.side_it) : __ldcg(c.sorted + p);  // see markpush
   EMB_TR_BEGIN(17, t);
   EMB_TR_WAITED(17, t);
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(MP_THREADS) marktag_kernel(DevCtx c, int p, in
 __global__ void __launch_bounds__(MP_THREADS) plan_kernel(DevCtx c, int p) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   const uint32_t t = __ldcg(c.sorted + p);  // t of this batch: sort(t) precedes on this stream (DESIGN B7)
   EMB_TR_BEGIN(19, t);
   EMB_TR_WAITED(19, t);
@@ -221,6 +224,7 @@ template <int EPT>
 __global__ void __launch_bounds__(RT_THREADS, 1) tables_kernel(DevCtx c, int p, int t_mode) {
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   __shared__ int s_tmp[64];
   __shared__ int s_tot[2];
   const int n = blockIdx.x;

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   constexpr int CS_WARPS = CS_THREADS / 32;
   EMB_TR_ENTRY();
   pdl_wait();
+  if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   cg::cluster_group cluster = cg::this_cluster();
   constexpr int SMAX = EPT * CS_THREADS;  // keys per CTA slice (max)
   constexpr int EPW = EPT * 32;           // keys per warp
