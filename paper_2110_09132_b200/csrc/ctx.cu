@@ -123,6 +123,7 @@ struct emb_ctx {
   bool sort_join = true;    // N == 1, prefetched: the forward waits for its sort's event (no GATE_SORTED kernel)
   bool fwd_joined = false;  // the last forward did
   bool fwd_dedup1 = false;  // N == 1 joined forward gathers each distinct row once per chunk (knob)
+  bool fwd_dedupn = true;   // N > 1 prefetched forward dedups when its sort is already complete (knob)
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
@@ -286,7 +287,9 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ctx->lc.fwd_bulk = env_int("EMB_FWD_BULK", big ? 1 : 0, 0, 1);
   }
   ctx->sort_join = env_int("EMB_SORT_JOIN", 1, 0, 1) != 0;
-  ctx->fwd_dedup1 = env_int("EMB_FWD_DEDUP1", 0, 0, 1) != 0;  // measured slower at N == 1 (profiles/r02_tune/next3.txt)
+  ctx->fwd_dedup1 = env_int("EMB_FWD_DEDUP1", 0, 0, 1) != 0;
+  // N > 1 forward dedup (measured: BERT N = 2 74.3 vs 80.4 us without; LM, GNMT within 1 us)
+  ctx->fwd_dedupn = env_int("EMB_FWD_DEDUPN", 1, 0, 1) != 0;  // measured slower at N == 1 (profiles/r02_tune/next3.txt)
 
   DevCtx& c = ctx->dc;
   memset(&c, 0, sizeof(c));
@@ -520,7 +523,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
   // (The forward's CTA 0 waiting for sort(t) instead of the GATE_SORTED
   // kernel measured GNMT -0.8 us, LM +2.9 us at N == 1 in round 1: a CTA
   // spinning in a wide kernel delays other streams' launches, §6 Liveness.)
-  const int dedup = (pre && ctx->pl.N > 1) ? 1 : 0;
+  const int dedup = (pre && ctx->pl.N > 1 && ctx->fwd_dedupn) ? 1 : 0;
   // N == 1, prefetched: sort(t) was launched by backward(t-1) one step ago.
   // The forward takes a real stream dependency on it (an event join: a graph
   // edge when captured) instead of a GATE_SORTED spin kernel before the
