@@ -57,6 +57,7 @@ struct DevCtx {
   int D, d, esz;          // esz: bytes per element of the table dtype
   int dtype, mode, optim;
   int max_tok;
+  int bypass;             // EMB_SINGLE_BYPASS: single-row uniques skip coal_reduce (apply reads dY)
   int pdl_early;          // EMB_PDL_EARLY: compute kernels trigger their dependents right after griddepcontrol.wait
   int cpr, cps;           // 16-byte chunks per full row (D*esz/16) / per column slice (d*esz/16)
   long long pad_id;
@@ -77,6 +78,7 @@ struct DevCtx {
   unsigned long long* slotmap;  // [2][L][N] (t << 32) | i — source n holds id as unique i at iteration t (N > 1)
   int* perm;              // [2][N][max_tok]    positions sorted by (dropped, id, position)
   int* uid;               // [2][N][max_tok]    ascending unique kept ids
+  int* upos;              // [2][N][max_tok]    single-row unique -> its position, else -1
   int* useg;              // [2][N][max_tok+1]  unique i -> first index into perm (useg[U] = end)
   int* chunk_off;         // [2][N][max_tok+1]  unique i -> first reduce chunk
   int4* chunk_desc;       // [2][N][max_chunks] chunk -> {unique i, perm begin, perm end, chunks of i}

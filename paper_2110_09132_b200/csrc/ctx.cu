@@ -98,7 +98,7 @@ emb_status make_plan(const emb_config* cfg, Plan* pl) {
   if (cfg->optim == EMB_ADAGRAD) loc += L * pl->d * 4;
   if (N > 1) loc += 2 * L * N * 8;                               // slotmap
   loc += 2 * L * 4;                                              // nextmark
-  loc += 3 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid slot_id | useg chunk_off
+  loc += 4 * 2 * N * T * 4 + 2 * 2 * N * (T + 1) * 4;            // perm uid upos slot_id | useg chunk_off
   loc += 2 * N * (size_t)pl->max_chunks * 16 + 2 * N * CNT_W * 4 + 2 * N * (size_t)pl->max_long * 4;
   if (cfg->mode != EMB_BWD_RAW) loc += T * cfg->dim * 4;       // gcoal
   loc += 2 * (size_t)pl->max_chunks * cfg->dim * 4;              // scratch
@@ -301,6 +301,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   c.scale = cfg->grad_scale != 0.f ? cfg->grad_scale : 1.0f / (float)pl.N;
   c.timeout_ns = (unsigned long long)(cfg->timeout_ms > 0 ? cfg->timeout_ms : 10000) * 1000000ull;
   c.pdl_early = env_int("EMB_PDL_EARLY", 0, 0, 1);
+  c.bypass = env_int("EMB_SINGLE_BYPASS", 1, 0, 1);
   c.C = pl.C; c.max_chunks = pl.max_chunks; c.max_long = pl.max_long; c.idbits = pl.idbits; c.posbits = pl.posbits;
   c.lay = pl.lay;
 
@@ -323,6 +324,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
     ALLOC(c.nextmark, 2 * L * 4);
     ALLOC(c.perm, 2 * N * T * 4);
     ALLOC(c.uid, 2 * N * T * 4);
+    ALLOC(c.upos, 2 * N * T * 4);
     ALLOC(c.useg, 2 * N * (T + 1) * 4);
     ALLOC(c.slot_id, 2 * N * T * 4);
     if (N > 1) ALLOC(c.plan, 2 * 2 * N * T * (1 + N) * 4);
@@ -707,7 +709,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       if (ctx->sort_join) CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_plan[p], 0));
       else CKC(ctx, gate(ctx, p, GATE_MARKED, 0, stream));
     }
-    CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, p, stream); }));
+    CKC(ctx, run_k(ctx, EMB_K_APPLY, stream, [&] { return launch_coal_apply(c, lc, grad_out, p, stream); }));
     // N == 1: the coalesce applied every row's update itself (one source = the
     // merged gradient); there is nothing to exchange or merge, for either part.
     if (mode == EMB_BWD_SPLIT && ctx->pl.N > 1) CKC(ctx, cudaEventRecord(ctx->ev_prior[p], stream));  // apply done

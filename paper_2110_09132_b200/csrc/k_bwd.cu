@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(BWD_THREADS) coal_reduce_kernel(DevCtx c, cons
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int ch = gw; ch < NCH; ch += nw) {
     const int4 dsc = desc[ch];  // {unique i, perm begin, perm end, chunks of i}
+    if (c.bypass && desc_pos1(dsc.w) >= 0) continue;  // single-row unique: the apply reads its dY row
     float acc[V * EPV];
     reduce_rows<DT, V, false>(dY, row_bytes, c.cpr, perm, dsc.y, dsc.z, acc, desc_pos1(dsc.w));
     store_partial<EPV, V>((desc_nch(dsc.w) > 1) ? part + (size_t)ch * c.D : c.gcoal + (size_t)dsc.x * c.D, c.cpr,
@@ -322,7 +323,8 @@ __device__ __forceinline__ void apply_store(const DevCtx& c, int p, uint32_t t, 
 static constexpr int SLICE = 128;  // fp32 columns per combine slice (one float4 per lane)
 
 template <int DT>
-__global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel(DevCtx c, int p) {
+__global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel(DevCtx c, const char* __restrict__ dY,
+                                                                                 int p) {
   EMB_TR_ENTRY();
   pdl_wait();
   if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
@@ -342,6 +344,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
   const size_t bpn = pn(c, p, r) * (size_t)c.max_tok;
   const int* uid = c.uid + bpn;
   const int* chunk_off = c.chunk_off + pn(c, p, r) * (size_t)(c.max_tok + 1);
+  const int* upos = c.upos + bpn;
   const int* long_u = c.long_u + pn(c, p, r) * (size_t)c.max_long;
   const float* part = c.scratch + (size_t)p * c.max_chunks * c.D;
 
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
   if (rl < RPB) {
     const int step = gridDim.x * RPB;
     for (int k0 = blockIdx.x * RPB + rl; k0 < U; k0 += step * EA) {
-      int kk[EA], id[EA];
+      int kk[EA], id[EA], up[EA];
       bool ok[EA];
       float g[EA][EPV];
       ApplyState<DT> st[EA];
@@ -412,16 +415,21 @@ __global__ void __launch_bounds__(BWD_THREADS, EMB_APPLY_MINB) coal_apply_kernel
         // uid and chunk_off loads issued together (uid[k] is valid for every k < U)
         const bool in = kk[j] < U;
         id[j] = in ? __ldcg(uid + kk[j]) : 0;
+        up[j] = (in && c.bypass) ? __ldcg(upos + kk[j]) : -1;
         ok[j] = in && (__ldcg(chunk_off + kk[j] + 1) - __ldcg(chunk_off + kk[j])) == 1;
       }
 #pragma unroll
       for (int j = 0; j < EA; ++j) {
         if (!ok[j]) continue;
-        const float* gp = c.gcoal + (size_t)kk[j] * c.D + c16 * EPV;
+        if (up[j] >= 0) {  // single-row unique: its sum is its dY row (exact in fp32)
+          Vec<DT>::unpack(ld16_nc(dY + (size_t)up[j] * ((size_t)c.D * c.esz) + (size_t)c16 * 16), g[j]);
+        } else {
+          const float* gp = c.gcoal + (size_t)kk[j] * c.D + c16 * EPV;
 #pragma unroll
-        for (int x = 0; x < EPV; x += 4) {
-          const float4 g4 = __ldcg(reinterpret_cast<const float4*>(gp + x));
-          g[j][x] = g4.x; g[j][x + 1] = g4.y; g[j][x + 2] = g4.z; g[j][x + 3] = g4.w;
+          for (int x = 0; x < EPV; x += 4) {
+            const float4 g4 = __ldcg(reinterpret_cast<const float4*>(gp + x));
+            g[j][x] = g4.x; g[j][x + 1] = g4.y; g[j][x + 2] = g4.z; g[j][x + 3] = g4.w;
+          }
         }
         apply_load<DT>(c, id[j], c16, st[j]);
       }
@@ -700,17 +708,18 @@ static cudaError_t coal_dispatch(const DevCtx& c, const LaunchCfg& L, const char
 }
 
 template <int DT>
-static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
+static cudaError_t apply_dispatch(const DevCtx& c, const LaunchCfg& L, const char* dY, int p, cudaStream_t s) {
   constexpr int EA = EMB_APPLY_EA(Vec<DT>::EPV);
   const int rpb = BWD_THREADS / c.cpr;
   long long grid = ((long long)c.max_tok + (long long)rpb * EA - 1) / ((long long)rpb * EA);
   if (grid > L.nsm * EMB_APPLY_GRID_PER_SM) grid = L.nsm * EMB_APPLY_GRID_PER_SM;
   if (grid < 1) grid = 1;
-  return launch_pdl(coal_apply_kernel<DT>, dim3((int)grid), dim3(BWD_THREADS), 0, s, c, p);
+  return launch_pdl(coal_apply_kernel<DT>, dim3((int)grid), dim3(BWD_THREADS), 0, s, c, dY, p);
 }
 
-cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s) {
-  return c.dtype == BF16 ? apply_dispatch<BF16>(c, L, p, s) : apply_dispatch<F32>(c, L, p, s);
+cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s) {
+  const char* y = static_cast<const char*>(dY);
+  return c.dtype == BF16 ? apply_dispatch<BF16>(c, L, y, p, s) : apply_dispatch<F32>(c, L, y, p, s);
 }
 
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, int gate_flags, cudaStream_t s) {

@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   int* chunk_off = c.chunk_off + pn(c, p, n) * (size_t)(c.max_tok + 1);
   int4* chunk_desc = c.chunk_desc + pn(c, p, n) * (size_t)c.max_chunks;
   int* long_u = c.long_u + pn(c, p, n) * (size_t)c.max_long;
+  int* upos = c.upos + bpn;
   const int hc = xs[0];  // this CTA's uniques: [kb, kb + hc)
   int my_ch = 0, my_long = 0;
   for (int j = tid; j < hc; j += CS_THREADS) {
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     if (j < hc) {
       const int off = cb + och;
       chunk_off[k] = off;
+      upos[k] = (b - a == 1) ? (int)(keyA[a - lo] & posmask) : -1;  // single-row unique: the apply reads dY there
       int qs = -1;
       if (nch > QMIN) {
         qs = atomicAdd(&xs[5], 1);

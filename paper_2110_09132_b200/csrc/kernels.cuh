@@ -109,7 +109,7 @@ cudaError_t launch_tables(const DevCtx& c, int p, int t_mode, cudaStream_t s);
 // stages scheduled rows.
 cudaError_t launch_coal(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, int gate_flags, cudaStream_t s);
 // a7 (multi-chunk combine) + a9/a10 or the N == 1 update: coalesced rows -> owners / stage / shard
-cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
+cudaError_t launch_coal_apply(const DevCtx& c, const LaunchCfg& L, const void* dY, int p, cudaStream_t s);
 // a12: push the staged scheduled rows to their owners (N > 1)
 cudaError_t launch_defpush(const DevCtx& c, const LaunchCfg& L, int p, cudaStream_t s);
 // RAW a7/a10: push raw dY column slices; owner-side per-source coalesce
