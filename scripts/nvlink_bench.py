@@ -47,6 +47,27 @@ def main():
         sent = per_pair * (world - 1)
         out["alltoall"].append({"bytes_per_pair": per_pair, "us": round(ms * 1e3, 2),
                                 "gbs_per_rank_out": round(sent / (ms * 1e-3) / 1e9, 1)})
+    # NCCL all_reduce of one dense block (bf16), the a13 queue's collective
+    out["allreduce"] = []
+    for mib in (4, 25, 100):
+        x = torch.ones((mib << 20) // 2, dtype=torch.bfloat16, device=dev)
+        for _ in range(5):
+            dist.all_reduce(x)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it = 20
+        e0.record()
+        for _ in range(it):
+            dist.all_reduce(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / it], device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        algbw = (mib << 20) / (ms * 1e-3) / 1e9
+        out["allreduce"].append({"mib_bf16": mib, "us": round(ms * 1e3, 1), "algbw_gbs": round(algbw, 1),
+                                 "busbw_gbs": round(algbw * 2 * (world - 1) / world, 1)})
     if rank == 0:
         out["note"] = ("alltoall gbs_per_rank_out = bytes each rank sends to its N-1 peers / time (the exchange's "
                        "per-GPU NVLink injection); nominal 900 GB/s per direction, guide-measured peer copy 770")
