@@ -805,6 +805,15 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    _align = torch.zeros(1, device=dev)
+
+    def device_align():
+        # N > 1: a one-element NCCL all_reduce on `stream` right before the start event, so that the
+        # ranks' timed regions start together on the device (the host barrier alone leaves the ranks'
+        # first launches up to ~0.3 ms apart, which a short run would count as exchange time)
+        if world > 1:
+            torch.distributed.all_reduce(_align)
+
     def check_err(phase):  # sticky device error bits (1 id range, 2 state, 4 peer-wait timeout)
         torch.cuda.synchronize()
         ef = ex.stats()["err_flags"]
@@ -820,7 +829,7 @@ def main():
     check_err("warm-up")
 
     # CUDA graph of one full cycle of nb steps (device-resident iteration counter -> replay-safe)
-    graph = None
+    graph = graph_rem = graph_comp = None
     k0 = args.warmup
     if not args.no_graph:
         try:
@@ -837,8 +846,35 @@ def main():
                 E.emb_join(ex.ctx, cap_stream)
             stream.wait_stream(cap_stream)
             graph = g
+            # K not a multiple of the cycle: the remaining steps (the first K mod nb of a cycle) are a
+            # graph too (graph_rem), with its complement (the other nb - rem steps of the cycle,
+            # graph_comp) so that both can be warmed up before the timed region as one full cycle,
+            # and the sequence closed after it (host and device stay one whole cycle apart: same
+            # batch, same parity).  Every timed step runs a captured, already-launched graph.
+            rem0 = args.steps % nb
+
+            def capture(j0, n):
+                gg = torch.cuda.CUDAGraph()
+                cap_stream.wait_stream(stream)
+                with torch.cuda.graph(gg, stream=cap_stream):
+                    for j in range(j0, j0 + n):
+                        b = (k0 + j) % nb
+                        if not args.graph_no_prefetch:
+                            E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], cap_stream)
+                        E.emb_forward_exchange(ex.ctx, ids_d[b], Y_d[b], cap_stream)
+                        E.emb_backward_exchange(ex.ctx, dY_d[b], ids_d[(b + 1) % nb], cap_stream)
+                    E.emb_join(ex.ctx, cap_stream)
+                stream.wait_stream(cap_stream)
+                return gg
+
+            if rem0 and os.environ.get("BENCH_GRAPH_REM", "1") != "0":
+                graph_rem = capture(0, rem0)
+                graph_comp = capture(rem0, nb - rem0)
             torch.cuda.synchronize()
             graph.replay()          # one untimed replay (it is also a warm-up cycle)
+            if graph_rem is not None:
+                graph_rem.replay()  # ... and one of the split cycle
+                graph_comp.replay()
             torch.cuda.synchronize()
         except Exception as e:  # pragma: no cover
             print(f"[bench] graph capture failed, timing eagerly: {e}", file=sys.stderr)
@@ -852,12 +888,22 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st0 = ex.stats() if world > 1 else None
     nv0 = nvlink_kib(local) if world > 1 else None
-    with ClockSampler(local) as clk:
+    clk = ClockSampler(local)  # NVML init here, outside the timed region (it takes milliseconds)
+    device_align()
+    # ~1 ms of device sleep queued ahead of the start event: the host enqueues the start event and the
+    # first replays while the device sleeps, so host launch latency (and the clock sampler's start)
+    # never shows up as idle device time inside the timed region; at N > 1 the ranks leave the sleep
+    # together (same cycle count after the aligning all_reduce)
+    torch.cuda._sleep(2_000_000)
+    with clk:
         ev0.record(stream)
         for _ in range(n_rep):
             graph.replay()
-        for j in range(rem):
-            step(k0 + j)
+        if graph_rem is not None:
+            graph_rem.replay()
+        else:
+            for j in range(rem):
+                step(k0 + j)
         E.emb_join(ex.ctx, stream)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -884,6 +930,9 @@ def main():
     if os.environ.get("EMB_TRACE_OUT"):  # kernel trace ring (EMB_TRACE builds; scripts/trace.py)
         np.save(f"{os.environ['EMB_TRACE_OUT']}.{rank}.npy", E.emb_debug_copy(ex.ctx, E.EMB_DBG_TIMESTAMPS))
     kk = k0 + rem                  # next batch index (graph replays are whole cycles)
+    if graph_rem is not None:      # close the split cycle (untimed)
+        graph_comp.replay()
+        kk = k0 + nb
     t_max = ms
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -912,6 +961,8 @@ def main():
             step(kk + j)
         kk += (k0 - kk) % nb
         barrier()
+        device_align()
+        torch.cuda._sleep(2_000_000)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
         evs[0].record(stream)
         for i in range(R):
@@ -1072,6 +1123,7 @@ def main():
     s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev = lambda: torch.cuda.Event()  # noqa: E731
     in_ready, done, out_done = {}, {}, {}
+    device_align()
     e0.record(stream)
     s_h2d.wait_event(e0)
     s_d2h.wait_event(e0)
