@@ -87,6 +87,9 @@ __device__ __forceinline__ void cluster_exsum(cg::cluster_group& cluster, int* s
   *all = a;
 }
 
+#ifndef EMB_SORT_SPREAD
+#define EMB_SORT_SPREAD 1
+#endif
 template <typename K, int EPT, int CL, int CS_THREADS>
 __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, const int* own_ids, int own_n,
                                                              int from_bwd) {
@@ -96,7 +99,6 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   cg::cluster_group cluster = cg::this_cluster();
   constexpr int SMAX = EPT * CS_THREADS;  // keys per CTA slice (max)
-  constexpr int EPW = EPT * 32;           // keys per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* keyA = reinterpret_cast<K*>(smem_raw);
   K* keyB = keyA + SMAX;
@@ -131,6 +133,10 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   const int S = (T + CL - 1) / CL;  // slice of each CTA (<= SMAX: T <= max_tok <= CL * SMAX)
   const int lo = cr * S;
   const int cnt = max(0, min(T, lo + S) - lo);
+  // keys per warp: the slice spread over all warps (ept <= EPT rounds of 32), so that the
+  // per-warp serial work (ranking, heads) is ept rounds, not EPT, when the batch is small
+  const int ept = EMB_SORT_SPREAD ? (S + CS_THREADS - 1) / CS_THREADS : EPT;
+  const int epw = ept * 32;
   const int posbits = c.posbits, idbits = c.idbits;
   const long long L = c.L;
 
@@ -169,7 +175,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     int dg[EPT], rk[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const int i = w * EPW + r * 32 + lane;
+      if (r >= ept) break;
+      const int i = w * epw + r * 32 + lane;
       const bool valid = i < cnt;
       const unsigned act = __ballot_sync(0xffffffffu, valid);
       dg[r] = 0;
@@ -205,7 +212,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const int i = w * EPW + r * 32 + lane;
+      if (r >= ept) break;
+      const int i = w * epw + r * 32 + lane;
       if (i < cnt) {
         const int P = gs[dg[r]] + wh[w][dg[r]] + rk[r];
         const int dst = P / S;
@@ -231,7 +239,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   int kept_heads = 0, kept_tok = 0, first_head = 0x7fffffff;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int i = w * EPW + r * 32 + lane;
+    if (r >= ept) break;
+    const int i = w * epw + r * 32 + lane;
     const bool valid = i < cnt;
     bool head = false, keep = false;
     if (valid) {
@@ -276,7 +285,8 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
     int kbase = wk[w];  // local unique index
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-      const int i = w * EPW + r * 32 + lane;
+      if (r >= ept) break;
+      const int i = w * epw + r * 32 + lane;
       const bool valid = i < cnt;
       bool head = false;
       K key = K(0);
