@@ -352,12 +352,16 @@ def _check_ints(rk, wl, k, res, pad_id, t):
                 f"iter {t} rank {r}: counts of {n}: {cnts[n]} vs T={len(ids_n)} u={res.u[n]} p={res.p[n]}"
 
 
-def graph_parity(cfg, N=1, mode="split", warm=3, nb=4, replays=2, device=0, colocated=False):
+def graph_parity(cfg, N=1, mode="split", warm=3, nb=4, replays=2, device=0, colocated=False, rem=0,
+                 graph_prefetch=False):
     """The bench's timed path: `warm` eager iterations (with emb_prefetch), one
     CUDA graph capturing a cycle of `nb` steps (forward + backward with next
-    ids) and emb_join, `replays` replays, one final eager iteration with
-    next_ids = NULL, flush — then the final shard / m / v against the oracle
-    run free over the same warm + replays * nb + 1 iterations."""
+    ids; `graph_prefetch`: + emb_prefetch per step, as bench.py) and emb_join,
+    `replays` replays, one final eager iteration with next_ids = NULL, flush —
+    then the final shard / m / v against the oracle run free over the same
+    iterations.  rem > 0: bench.py's short-run path — the cycle also split
+    into a graph of its first `rem` steps and one of the other nb - rem,
+    replayed as: cycle, rem, rest (warm-up), `replays` cycles, rem, rest."""
     import torch
     assert nb % 2 == 0
     dev = torch.device("cuda", device)
@@ -390,22 +394,40 @@ def graph_parity(cfg, N=1, mode="split", warm=3, nb=4, replays=2, device=0, colo
         for r, ex, s in rk.items():
             E.emb_join(ex.ctx, s)
         torch.cuda.synchronize()
-        graphs = []
-        for r, ex, s in rk.items():
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
-                for j in range(nb):
-                    b = (warm + j) % nb
-                    E.emb_forward_exchange(ex.ctx, ids_d[r][b], Y_d[r][b], s)
-                    E.emb_backward_exchange(ex.ctx, dY_d[r][b], ids_d[r][(b + 1) % nb], s)
-                E.emb_join(ex.ctx, s)
-            graphs.append((g, s))
-        torch.cuda.synchronize()
-        for _ in range(replays):
-            for g, s in graphs:
+        def capture(j0, n):
+            out = []
+            for r, ex, s in rk.items():
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    for j in range(j0, j0 + n):
+                        b = (warm + j) % nb
+                        if graph_prefetch:
+                            E.emb_prefetch(ex.ctx, ids_d[r][(b + 1) % nb], s)
+                        E.emb_forward_exchange(ex.ctx, ids_d[r][b], Y_d[r][b], s)
+                        E.emb_backward_exchange(ex.ctx, dY_d[r][b], ids_d[r][(b + 1) % nb], s)
+                    E.emb_join(ex.ctx, s)
+                out.append((g, s))
+            return out
+
+        def replay(gs, j0, n):
+            for g, s in gs:
                 with torch.cuda.stream(s):      # replay() launches on the CURRENT stream
                     g.replay()
-            seq.extend((warm + j) % nb for j in range(nb))
+            seq.extend((warm + j) % nb for j in range(j0, j0 + n))
+
+        graphs = capture(0, nb)
+        if rem:
+            g_rem, g_comp = capture(0, rem), capture(rem, nb - rem)
+        torch.cuda.synchronize()
+        if rem:
+            replay(graphs, 0, nb)
+            replay(g_rem, 0, rem)
+            replay(g_comp, rem, nb - rem)
+        for _ in range(replays):
+            replay(graphs, 0, nb)
+        if rem:
+            replay(g_rem, 0, rem)
+            replay(g_comp, rem, nb - rem)
         b = (warm + replays * nb) % nb
         for r, ex, s in rk.items():
             ex.forward(ids_d[r][b], Y_d[r][b], s)

@@ -91,6 +91,11 @@ def test_graph_replay_colocated():
     graph_parity(_small("gnmt", 8), N=2, colocated=True)
 
 
+def test_graph_split_cycle_colocated():
+    """bench.py's short-run graph path (cycle split in rem + rest), two co-located ranks."""
+    graph_parity(_small("gnmt", 8), N=2, colocated=True, rem=1, graph_prefetch=True)
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_adagrad_colocated(n):
     parity_run(get_config("tiny"), N=n, mode="split", iters=3, optim="adagrad", lr=0.05, colocated=True)

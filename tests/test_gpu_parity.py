@@ -189,6 +189,15 @@ def test_graph_replay_n1(name):
     assert iters == 3 + 2 * 4 + 1
 
 
+@pytest.mark.parametrize("rem", [1, 3])
+def test_graph_split_cycle_n1(rem):
+    """bench.py's short-run path: the cycle also captured as a graph of its first
+    `rem` steps plus one of the rest (warmed as one cycle, closed after the
+    timed replays), emb_prefetch inside the graphs — final state vs the oracle."""
+    errs, iters = graph_parity(get_config("tiny"), N=1, nb=4, rem=rem, graph_prefetch=True)
+    assert iters == 3 + (2 + 2) * 4 + 1
+
+
 @pytest.mark.slow
 def test_graph_replay_lm_full_size():
     """BASELINE configs[1] at full size through the graph path bench.py times."""
