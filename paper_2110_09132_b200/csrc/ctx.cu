@@ -135,6 +135,8 @@ struct emb_ctx {
   cudaEvent_t ev_marked = nullptr, ev_join_aux = nullptr, ev_join_side = nullptr, ev_join_aux2 = nullptr;
   bool mark_pending = false;  // N == 1: mark runs on the side stream; the next forward checks its pushed ids
   bool aux_used = false, side_used = false;  // since the last emb_join
+  bool aux2_used = false;  // N == 1: a sort went to aux2 since the last emb_join (a capture that never
+                           // forked aux2 must not join it: that would depend on uncaptured work)
   long long it = 0;          // forward calls so far (host mirror of the device t)
   long long bwd_done = 0;
   bool prefetched = false;   // last backward pushed next ids
@@ -549,6 +551,7 @@ emb_status emb_forward_exchange(emb_ctx* ctx, const int32_t* ids, int32_t n, voi
     // forward pushed them; the sort publishes the push to the peers)
     CKC(ctx, cudaEventRecord(ctx->ev_main[p], stream));
     cudaStream_t sq = (ctx->pl.N == 1 && (p & 1)) ? ctx->aux2 : ctx->aux;
+    if (sq == ctx->aux2) ctx->aux2_used = true;
     CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_main[p], 0));
     CKC(ctx, gate(ctx, p, GATE_SORT, 1 | 2 | 4, sq));
     CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
@@ -639,6 +642,7 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       // the sort of t+1 goes to the stream of its parity: consecutive sorts may
       // overlap (each is one 8-SM cluster), so the sort no longer bounds the step
       cudaStream_t sq = ((p ^ 1) & 1) ? ctx->aux2 : aux;
+      if (sq == ctx->aux2) ctx->aux2_used = true;
       CKC(ctx, cudaStreamWaitEvent(sq, fork, 0));
       if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_tables[p ^ 1], 0));
       CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
@@ -801,11 +805,12 @@ emb_status emb_join(emb_ctx* ctx, emb_stream_t stream_) {
   if (ctx->aux_used) {
     CKC(ctx, cudaEventRecord(ctx->ev_join_aux, ctx->aux));
     CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux, 0));
-    if (ctx->pl.N == 1) {
-      CKC(ctx, cudaEventRecord(ctx->ev_join_aux2, ctx->aux2));
-      CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux2, 0));
-    }
     ctx->aux_used = false;
+  }
+  if (ctx->aux2_used) {
+    CKC(ctx, cudaEventRecord(ctx->ev_join_aux2, ctx->aux2));
+    CKC(ctx, cudaStreamWaitEvent(stream, ctx->ev_join_aux2, 0));
+    ctx->aux2_used = false;
   }
   if (ctx->side_used) {
     CKC(ctx, cudaEventRecord(ctx->ev_join_side, ctx->side));

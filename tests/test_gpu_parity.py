@@ -195,7 +195,7 @@ def test_graph_split_cycle_n1(rem):
     `rem` steps plus one of the rest (warmed as one cycle, closed after the
     timed replays), emb_prefetch inside the graphs — final state vs the oracle."""
     errs, iters = graph_parity(get_config("tiny"), N=1, nb=4, rem=rem, graph_prefetch=True)
-    assert iters == 3 + (2 + 2) * 4 + 1
+    assert iters == 3 + (1 + 1 + 2 + 1) * 4 + 1  # warm cycle, warm split cycle, 2 replays, closing split cycle
 
 
 @pytest.mark.slow
