@@ -127,7 +127,9 @@ struct emb_ctx {
   std::vector<void*> allocs;
   cudaStream_t side = nullptr;  // scheduled part (lowest priority)
   cudaStream_t aux = nullptr;   // sort of the next batch; N > 1 also prefetch push + D_next tags + tables
-  cudaStream_t aux2 = nullptr;  // N == 1: the sorts of odd batches (two sorts may overlap; 8 SMs each)
+  cudaStream_t aux2 = nullptr;  // N == 1: the sorts of odd batches (two sorts may overlap; 8 SMs each);
+                                // N > 1 (EMB_SORT_STREAM, one GPU per process): every prefetched sort
+  cudaEvent_t ev_gsort = nullptr;  // N > 1: ids of the next batch gathered (aux) -> its sort (aux2)
   cudaEvent_t ev_prior[2] = {}, ev_def[2] = {}, ev_main[2] = {}, ev_sorted[2] = {}, ev_tables[2] = {}, ev_plan[2] = {};
   bool def_pending[2] = {false, false};
   bool sort_pending[2] = {false, false};
@@ -383,6 +385,7 @@ emb_status emb_create(const emb_config* cfg, emb_ctx** out) {
   if (cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_aux, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_aux2, cudaEventDisableTiming) != cudaSuccess) goto fail;
+  if (cudaEventCreateWithFlags(&ctx->ev_gsort, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaEventCreateWithFlags(&ctx->ev_join_side, cudaEventDisableTiming) != cudaSuccess) goto fail;
   if (cudaDeviceSynchronize() != cudaSuccess) goto fail;
   *out = ctx;
@@ -494,6 +497,18 @@ emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8
   int err = 0;
   CKC(ctx, cudaMemcpy(&err, ctx->dc.err, 4, cudaMemcpyDeviceToHost));
   if (err & ERR_TIMEOUT) { ctx->poisoned = EMB_ERR_TIMEOUT; return EMB_ERR_TIMEOUT; }
+  // N > 1, one GPU per process: the prefetched sort of the next batch on a
+  // stream of its own (EMB_SORT_STREAM), forked from aux right after the ids
+  // gate, so the aux chain (tags, merge plan) no longer waits behind it.  Pays
+  // where that chain bounds the step: a 3-pass sort (vocabulary > 2^16 ids) at
+  // N >= 4 (LM N = 4 52.7 -> 46.9 us); slower at N = 2 and for the 2-pass
+  // 32K vocabularies (GNMT N = 4 +2 us) — profiles/r02_tune/sort_stream.txt.
+  // Not for co-located ranks, which keep <= 3 streams each.
+  if (ctx->pl.N > 1 && env_int("EMB_SORT_STREAM", (ctx->pl.N >= 4 && ctx->pl.idbits > 16) ? 1 : 0, 0, 1)) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CKC(ctx, cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, hi));
+  }
   if (nccl_id) {
     ctx->dq = dense_queue_create(nccl_id, ctx->pl.N, ctx->pl.r, ctx->cfg.queue_window);
     if (!ctx->dq) { ctx->poisoned = EMB_ERR_NCCL; return EMB_ERR_NCCL; }
@@ -677,13 +692,27 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
     // next_ids == NULL (D_next = ∅): nothing is pushed or published for batch
     // t+1 here — forward(t+1) pushes, publishes and sorts its own ids — so the
     // gate only keeps the wait that frees parity p's tags / plan (flag 8)
+    // (sort stream aux2: the aux chain reads sort(t)'s lists and epoch, so it
+    // first joins sort(t); the sort of t+1 forks from aux right after the gate)
+    const bool s2 = ctx->aux2 != nullptr;
+    if (s2 && ctx->sort_pending[p]) CKC(ctx, cudaStreamWaitEvent(aux, ctx->ev_sorted[p], 0));
     if (next_ids) CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_markpush(c, p, next_ids, n_next, 0, aux); }));
     CKC(ctx, gate(ctx, p ^ 1, GATE_SORT, next_ids ? (1 | 2 | 4 | 8 | 16) : (8 | 16), aux));
+    if (next_ids && s2) {
+      CKC(ctx, cudaEventRecord(ctx->ev_gsort, aux));
+      CKC(ctx, cudaStreamWaitEvent(ctx->aux2, ctx->ev_gsort, 0));
+      ctx->aux2_used = true;
+      CKC(ctx, run_k(ctx, EMB_K_SORT, ctx->aux2, [&] {
+        return launch_sort(c, p ^ 1, nullptr, 0, 1, ctx->pl.key64, ctx->pl.sort_smem, ctx->aux2);
+      }));
+      CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], ctx->aux2));
+      ctx->sort_pending[p ^ 1] = true;
+    }
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_marktag(c, p, do_mark, 0, 0, aux); }));
     CKC(ctx, cudaEventRecord(ctx->ev_plan[p], aux));  // D_next tags of t+1 complete (the apply routes by them)
     CKC(ctx, run_k(ctx, EMB_K_ROUTE, aux, [&] { return launch_plan(c, p, aux); }));
     ctx->aux_used = true;
-    if (next_ids) {
+    if (next_ids && !s2) {
       CKC(ctx, run_k(ctx, EMB_K_SORT, aux, [&] {
         return launch_sort(c, p ^ 1, nullptr, 0, 1, ctx->pl.key64, ctx->pl.sort_smem, aux);
       }));
@@ -1003,7 +1032,8 @@ emb_status emb_shard_destroy(emb_ctx* ctx) {
     if (ctx->ev_tables[i]) cudaEventDestroy(ctx->ev_tables[i]);
     if (ctx->ev_plan[i]) cudaEventDestroy(ctx->ev_plan[i]);
   }
-  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre, ctx->ev_join_aux2}) {
+  for (cudaEvent_t e : {ctx->ev_marked, ctx->ev_join_aux, ctx->ev_join_side, ctx->ev_pre, ctx->ev_join_aux2,
+                        ctx->ev_gsort}) {
     if (e) cudaEventDestroy(e);
   }
   delete ctx;
