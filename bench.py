@@ -828,7 +828,11 @@ def main():
     E.emb_join(ex.ctx, stream)
     check_err("warm-up")
 
-    # CUDA graph of one full cycle of nb steps (device-resident iteration counter -> replay-safe)
+    # CUDA graph of G steps = whole cycles of the nb batches (device-resident iteration counter ->
+    # replay-safe).  A graph ends with emb_join, which drains the pipeline (the next batch's sort,
+    # the last step's deferred part); G >= 64 steps makes that drain one per >= 64 steps, as in a
+    # training loop that never joins, instead of one per cycle of nb.
+    G = nb * max(1, 64 // nb)
     graph = graph_rem = graph_comp = None
     k0 = args.warmup
     if not args.no_graph:
@@ -837,7 +841,7 @@ def main():
             cap_stream = torch.cuda.Stream()
             cap_stream.wait_stream(stream)
             with torch.cuda.graph(g, stream=cap_stream):
-                for j in range(nb):
+                for j in range(G):
                     b = (k0 + j) % nb
                     if not args.graph_no_prefetch:   # the paper's prefetch, as in step()
                         E.emb_prefetch(ex.ctx, ids_d[(b + 1) % nb], cap_stream)
@@ -846,12 +850,12 @@ def main():
                 E.emb_join(ex.ctx, cap_stream)
             stream.wait_stream(cap_stream)
             graph = g
-            # K not a multiple of the cycle: the remaining steps (the first K mod nb of a cycle) are a
-            # graph too (graph_rem), with its complement (the other nb - rem steps of the cycle,
+            # K not a multiple of G: the remaining steps (the first K mod G of the graph's sequence) are a
+            # graph too (graph_rem), with its complement (the other G - rem steps,
             # graph_comp) so that both can be warmed up before the timed region as one full cycle,
             # and the sequence closed after it (host and device stay one whole cycle apart: same
             # batch, same parity).  Every timed step runs a captured, already-launched graph.
-            rem0 = args.steps % nb
+            rem0 = args.steps % G
 
             def capture(j0, n):
                 gg = torch.cuda.CUDAGraph()
@@ -869,7 +873,7 @@ def main():
 
             if rem0 and os.environ.get("BENCH_GRAPH_REM", "1") != "0":
                 graph_rem = capture(0, rem0)
-                graph_comp = capture(rem0, nb - rem0)
+                graph_comp = capture(rem0, G - rem0)
             torch.cuda.synchronize()
             graph.replay()          # one untimed replay (it is also a warm-up cycle)
             if graph_rem is not None:
@@ -882,7 +886,7 @@ def main():
 
     # ---------------- timed region
     K = args.steps
-    n_rep, rem = (divmod(K, nb) if graph is not None else (0, K))
+    n_rep, rem = (divmod(K, G) if graph is not None else (0, K))
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -932,7 +936,7 @@ def main():
     kk = k0 + rem                  # next batch index (graph replays are whole cycles)
     if graph_rem is not None:      # close the split cycle (untimed)
         graph_comp.replay()
-        kk = k0 + nb
+        kk = k0 + G
     t_max = ms
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -953,7 +957,7 @@ def main():
         return tt.tolist()
 
     dist_t = {}
-    R = max(4, min(64, K // max(nb, 1)))
+    R = max(4, min(64, K // max(G, 1)))
     if graph is not None:
         # realign the batch sequence with the captured cycle (the graph's first
         # forward expects the ids promised by the step before it)
@@ -969,7 +973,7 @@ def main():
             graph.replay()
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
-        per = _max_over_ranks([evs[i].elapsed_time(evs[i + 1]) * 1e3 / nb for i in range(R)])
+        per = _max_over_ranks([evs[i].elapsed_time(evs[i + 1]) * 1e3 / G for i in range(R)])
         dist_t["graph"] = {"mean_us": round(statistics.mean(per), 3), "median_us": round(statistics.median(per), 3),
                            "samples": R, "unit": "us per step (per-replay events / steps per replay)"}
     Ee = min(K, 400)
@@ -1228,7 +1232,7 @@ def main():
                        "mode": mode, "optim": cfg.optim, "parallelism": f"column-shard x{world}",
                        "batches_cycled": nb, "l2": f"rotating {nb} batches (inputs+outputs "
                        f"{nb * 2 * cfg.max_tokens * cfg.D * (2 if cfg.dtype == 'bf16' else 4) / 2**20:.0f} MiB > 126 MiB L2)",
-                       "cuda_graph": graph is not None, "tokens_counted": "non-pad (id 0 = pad)"},
+                       "cuda_graph": graph is not None, "graph_steps": G if graph is not None else 0, "tokens_counted": "non-pad (id 0 = pad)"},
             "roofline": roof,
             "step_roofline": {"t_roof_us": round(t_roof_us, 3), "t_step_us": round(ms_per_step * 1e3, 3),
                               "frac": round(t_roof_us / (ms_per_step * 1e3), 4),
