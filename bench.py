@@ -832,7 +832,7 @@ def main():
     # replay-safe).  A graph ends with emb_join, which drains the pipeline (the next batch's sort,
     # the last step's deferred part); G >= 64 steps makes that drain one per >= 64 steps, as in a
     # training loop that never joins, instead of one per cycle of nb.
-    G = nb * max(1, 64 // nb)
+    G = nb * max(1, int(os.environ.get("BENCH_GRAPH_MIN_STEPS", "64")) // nb)
     graph = graph_rem = graph_comp = None
     k0 = args.warmup
     if not args.no_graph:
