@@ -500,11 +500,11 @@ emb_status emb_shard_init(emb_ctx* ctx, const uint8_t* peer_handles, const uint8
   // N > 1, one GPU per process: the prefetched sort of the next batch on a
   // stream of its own (EMB_SORT_STREAM), forked from aux right after the ids
   // gate, so the aux chain (tags, merge plan) no longer waits behind it.  Pays
-  // where that chain bounds the step: a 3-pass sort (vocabulary > 2^16 ids) at
-  // N >= 4 (LM N = 4 52.7 -> 46.9 us); slower at N = 2 and for the 2-pass
-  // 32K vocabularies (GNMT N = 4 +2 us) — profiles/r02_tune/sort_stream.txt.
+  // where that chain bounds the step, at N >= 4 (steady state, N = 4: LM 52.7
+  // -> 46.9 us, BERT 91 -> 73 us, GNMT / Transformer neutral); mixed at N = 2,
+  // so off there — profiles/r02_tune/sort_stream.txt.
   // Not for co-located ranks, which keep <= 3 streams each.
-  if (ctx->pl.N > 1 && env_int("EMB_SORT_STREAM", (ctx->pl.N >= 4 && ctx->pl.idbits > 16) ? 1 : 0, 0, 1)) {
+  if (ctx->pl.N > 1 && env_int("EMB_SORT_STREAM", ctx->pl.N >= 4 ? 1 : 0, 0, 1)) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     CKC(ctx, cudaStreamCreateWithPriority(&ctx->aux2, cudaStreamNonBlocking, hi));

@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02ss4; mkdir -p $O
+bash scripts/gpu_multi_exp.sh $O 4 "bert_large gnmt transformer" "EMB_SORT_STREAM=0" "EMB_SORT_STREAM=1" "EMB_SORT_STREAM=0" "EMB_SORT_STREAM=1" > /dev/null
+bash scripts/gpu_multi_exp.sh $O 2 "bert_large" "EMB_SORT_STREAM=0" "EMB_SORT_STREAM=1" > /dev/null
+cat $O/summary.txt
