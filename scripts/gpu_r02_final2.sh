@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"
-O=gpurun_out/r02_end3; mkdir -p $O
+O=${1:-gpurun_out/r02_end3}; mkdir -p $O
 bash scripts/gpu_roundend.sh $O
 timeout 300 python bench.py --steps 20 --warmup 3 > $O/bench_k20.json 2> $O/bench_k20.err; echo "bench k20 rc=$?" >> $O/rc.txt
 cat $O/rc.txt
