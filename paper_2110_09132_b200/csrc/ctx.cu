@@ -595,6 +595,9 @@ emb_status emb_prefetch(emb_ctx* ctx, const int32_t* next_ids, int32_t n_next, e
   return EMB_OK;
 }
 
+#ifndef EMB_SORT_QUIET
+#define EMB_SORT_QUIET 1  // N == 1 joined prefetch sorts skip the flag fences (see k_sort.cu)
+#endif
 emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32_t* next_ids, int32_t n_next,
                                  emb_stream_t stream_) {
   emb_status st = ctx_check(ctx);
@@ -661,7 +664,8 @@ emb_status emb_backward_exchange(emb_ctx* ctx, const void* grad_out, const int32
       CKC(ctx, cudaStreamWaitEvent(sq, fork, 0));
       if (ctx->tables_pending[p ^ 1]) CKC(ctx, cudaStreamWaitEvent(sq, ctx->ev_tables[p ^ 1], 0));
       CKC(ctx, run_k(ctx, EMB_K_SORT, sq, [&] {
-        return launch_sort(c, p ^ 1, next_ids, n_next, 2, ctx->pl.key64, ctx->pl.sort_smem, sq);
+        return launch_sort(c, p ^ 1, next_ids, n_next, ctx->sort_join && EMB_SORT_QUIET ? 3 : 2, ctx->pl.key64,
+                           ctx->pl.sort_smem, sq);
       }));
       CKC(ctx, cudaEventRecord(ctx->ev_sorted[p ^ 1], sq));
       ctx->sort_pending[p ^ 1] = true;

@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   pdl_wait();
   if (c.pdl_early) pdl_trigger();  // EMB_PDL_EARLY: let the dependent grid launch now
   cg::cluster_group cluster = cg::this_cluster();
+  // from_bwd == 3: an N == 1 prefetched sort whose forward joins its event —
+  // no device flag consumer, so its completion count needs no fences
+  const bool quiet = from_bwd == 3;
+  if (quiet) from_bwd = 2;
   constexpr int SMAX = EPT * CS_THREADS;  // keys per CTA slice (max)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* keyA = reinterpret_cast<K*>(smem_raw);
@@ -394,7 +398,9 @@ __global__ void __launch_bounds__(CS_THREADS) csort_kernel(DevCtx c, int p, cons
   }
   EMB_TR_AT(1, tt, 7);
   cluster.sync();  // no CTA exits while a peer may still read its shared memory
-  if (cr == 0 && tid == 0) {
+  if (quiet) {
+    if (cr == 0 && tid == 0) atomicAdd(&c.sort_count[p], 1u);  // trace labels / later GATE_SORTED counts
+  } else if (cr == 0 && tid == 0) {
     // sort of parity p complete once every source's cluster arrived: the gate
     // before the coalesce waits for sorted[p] (no host event on the main stream)
     __threadfence();
