@@ -305,11 +305,13 @@ __global__ void __launch_bounds__(FB_THREADS) fwd_bulk_kernel(DevCtx c, const in
   pdl_trigger();
 }
 
+// rows per stage x CTAs per SM: 4 x 8 measured best for the LM (19.75 vs 19.92 us
+// per step with 16 x 3; forward span 4.0 vs 4.5 us — profiles/r02_tune/fwd_bulk.txt)
 #ifndef EMB_FWD_BULK_ROWS
-#define EMB_FWD_BULK_ROWS 16
+#define EMB_FWD_BULK_ROWS 4
 #endif
 #ifndef EMB_FWD_BULK_PER_SM
-#define EMB_FWD_BULK_PER_SM 3
+#define EMB_FWD_BULK_PER_SM 8
 #endif
 static int fwd_bulk_rows(const DevCtx& c) {
   int R = EMB_FWD_BULK_ROWS;  // rows per stage (one per lane of warp 0)
