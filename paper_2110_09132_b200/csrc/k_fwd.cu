@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(DevCtx c, const int* _
 // cp.async.bulk shared -> global; two stages, so the loads of batch i+1 are in
 // flight while batch i drains.  Invalid ids get a zero row (generic stores)
 // and the sticky ERR_ID, as in fwd_kernel.
-static constexpr int FB_THREADS = 128;
+#ifndef EMB_FWD_BULK_THREADS
+#define EMB_FWD_BULK_THREADS 128
+#endif
+static constexpr int FB_THREADS = EMB_FWD_BULK_THREADS;
 static constexpr int FB_STAGES = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
